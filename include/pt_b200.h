@@ -1,0 +1,176 @@
+/*
+ * pt_b200.h -- C ABI of the B200-native online polarized-traces solve.
+ *
+ * This is the drop-in boundary for the reference's online GMRES stage
+ * (helmsweep, arXiv 1410.5910).  Every entry point below replaces one
+ * reference interface; the citation is file:line in the reference package
+ * (pkg/src/helmsweep/).  Plain C types only: complex numbers are
+ * interleaved (re, im) doubles, layout-identical to numpy complex128 and
+ * cuDoubleComplex.  Vectors passed to the apply/solve calls are DEVICE
+ * pointers (cudaMalloc'd, or torch CUDA tensors' data_ptr()); the upload
+ * arrays of pt_create and the *_host calls take HOST pointers.
+ *
+ * All functions return 0 on success, PT_EINVAL (-1) for a shape/layout
+ * error (the reference raises ValueError) and PT_ECUDA (-2) for a CUDA
+ * failure, PT_ENONFINITE (-3) when GMRES meets non-finite values (the
+ * reference raises RuntimeError, solver.py:255-258); pt_last_error()
+ * returns the message of the last failure on the calling thread.
+ *
+ * Calls are stream-ordered on the given stream (NULL = legacy default);
+ * a handle must not be used from two threads at once.
+ */
+#ifndef PT_B200_H
+#define PT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PT_ABI_VERSION 1
+
+#define PT_OK 0
+#define PT_EINVAL (-1)
+#define PT_ECUDA (-2)
+#define PT_ENONFINITE (-3)
+
+typedef void *pt_stream; /* a cudaStream_t */
+typedef struct pt_handle pt_handle;
+typedef struct pt_gmres_ws pt_gmres_ws;
+
+/* Kernel storage formats of BlockEntry.kernel (trace_system.py:145-150). */
+#define PT_KERNEL_DENSE 0 /* ndarray: m x m row-major complex128        */
+#define PT_KERNEL_PLR 1   /* PLRSparseForm: quadtree leaves (plr.py:239) */
+
+/* Shape of the polarized ("jump") interface system
+ * (trace_system.py:368-472): n_block_rows = 2*nt block rows and columns of
+ * m x m blocks, nt = 2L-2 trace blocks per half. */
+typedef struct {
+  int64_t m;            /* interface width nx + 2*n_pml                  */
+  int64_t n_block_rows; /* 2*nt; must be even                            */
+  int32_t kernel_format;/* PT_KERNEL_DENSE or PT_KERNEL_PLR              */
+  int32_t n_kernels;    /* distinct kernel objects shared by the entries */
+} pt_layout;
+
+/* One BlockEntry: y[row] += scale * K[kernel] @ x[col] + eye * x[col]
+ * (trace_system.py:159-168); kernel = -1 is a pure identity entry. */
+typedef struct {
+  int64_t row, col, kernel;
+  double scale_re, scale_im;
+  double eye_re, eye_im;
+} pt_entry;
+
+/* One PLR leaf (plr.py:58-75) of kernel `kernel`, at block offset
+ * (row_off, col_off) of size rows x cols and rank `rank`.  Its factors live
+ * in the factor array: U*Sigma is rows x rank row-major at u_off, Vt is
+ * rank x cols row-major at vt_off (offsets in complex elements).  Leaves
+ * of one kernel must tile its m x m block; rank-0 leaves may be omitted. */
+typedef struct {
+  int64_t kernel, row_off, col_off, rows, cols, rank, u_off, vt_off;
+} pt_leaf;
+
+/* GmresConfig (solver.py:71-80) + PreconditionerConfig.n_it (:59-68). */
+typedef struct {
+  double rel_tol;   /* converged when rel residual <= rel_tol           */
+  int32_t max_iter; /* no restart (solver.py:231)                        */
+  int32_t n_it;     /* Gauss-Seidel sweeps per preconditioner apply      */
+} pt_gmres_config;
+
+/* Flags of SolveReport.flag (solver.py:96-107, :265-289). */
+#define PT_FLAG_CONVERGED 0
+#define PT_FLAG_BREAKDOWN 1
+#define PT_FLAG_STAGNATION 2
+#define PT_FLAG_MAXITER 3
+
+/* SolveReport subset filled by the device solve.  residual_history must
+ * point to max_iter doubles (host memory) or be NULL. */
+typedef struct {
+  int32_t iterations;
+  int32_t flag;
+  int32_t converged;
+  int32_t nonfinite; /* 1 if GMRES stopped on a non-finite apply */
+  double true_residual;
+  double beta;       /* ||M^-1 b|| */
+  double *residual_history;
+} pt_report;
+
+/* ---- operator handle ----------------------------------------------------
+ * Upload the offline operator once (replaces OfflineState.pol/perm/d/r,
+ * solver.py:110-129, built by assemble_polarized + split_DR,
+ * trace_system.py:368-524).  dense: n_kernels*m*m complex (host) or NULL;
+ * leaves/factors: PLR tables (host) or NULL.  perm is sweep_permutation
+ * (trace_system.py:353-365) in natural block-row indices. */
+int pt_create(const pt_layout *layout, const pt_entry *entries,
+              int64_t n_entries, const int64_t *perm, const double *dense,
+              const pt_leaf *leaves, int64_t n_leaves, const double *factors,
+              int64_t n_factor_complex, int device, pt_handle **out);
+int pt_destroy(pt_handle *h);
+
+/* y = pol @ x   (BlockInterfaceMatrix.matvec, trace_system.py:219-226). */
+int pt_apply_A(pt_handle *h, const double *x, double *y, pt_stream stream);
+
+/* z = preconditioner_apply(n_it sweeps from zero)  (solver.py:223-228). */
+int pt_apply_M(pt_handle *h, const double *r, double *z, int32_t n_it,
+               pt_stream stream);
+
+/* u_out = D^-1 (P rhs - R u_in)   (gs_sweep, solver.py:203-220). */
+int pt_gs_sweep(pt_handle *h, const double *rhs, const double *u_in,
+                double *u_out, pt_stream stream);
+
+/* Left-preconditioned GMRES on the device: x = solution, report filled
+ * (gmres_solve, solver.py:231-295, with CGS2 + Givens in place of MGS +
+ * lstsq).  b, x device pointers.  Synchronises the stream once. */
+int pt_gmres(pt_handle *h, const double *b, double *x,
+             const pt_gmres_config *cfg, pt_report *report, pt_stream stream);
+
+/* Same with HOST b/x: the H2D copy, the solve and the D2H copy all happen
+ * inside (the gmres stage of solve_helmholtz, solver.py:376-397). */
+int pt_gmres_host(pt_handle *h, const double *b_host, double *x_host,
+                  const pt_gmres_config *cfg, pt_report *report,
+                  pt_stream stream);
+
+/* Batched independent solves of nrhs right-hand sides stored column after
+ * column (b[s*N ...]); reports[s] per RHS.  Operator applies become
+ * multi-RHS contractions (no reference API; cli.py:380-409 loops). */
+int pt_gmres_batch(pt_handle *h, const double *b, double *x, int32_t nrhs,
+                   const pt_gmres_config *cfg, pt_report *reports,
+                   pt_stream stream);
+
+/* ---- generic GMRES workspace (callable operators) ------------------------
+ * The reference's gmres_solve takes arbitrary callables apply_A/apply_Minv.
+ * These entry points run the device Arnoldi/Givens machinery while the
+ * caller applies its own operators between steps. */
+int pt_gmres_ws_create(int64_t n, int32_t max_iter, int device,
+                       pt_gmres_ws **out);
+int pt_gmres_ws_destroy(pt_gmres_ws *ws);
+/* device pointer to basis column j (length n), for the caller's applies */
+double *pt_gmres_ws_basis(pt_gmres_ws *ws, int32_t j);
+/* mb = M^-1 b already computed by the caller: beta = ||mb||, V0 = mb/beta.
+ * *beta_out receives beta (0 => x = 0, converged). */
+int pt_gmres_ws_begin(pt_gmres_ws *ws, const double *mb, double *beta_out,
+                      pt_stream stream);
+/* w = M^-1 A v_j has been written to basis column j+1 by the caller:
+ * CGS2 + Givens + flags.  *stop_out = 1 when the loop must end; status
+ * fields land in the report (residual_history appended). */
+int pt_gmres_ws_step(pt_gmres_ws *ws, int32_t j, double rel_tol,
+                     int32_t max_iter, pt_report *report, int32_t *stop_out,
+                     pt_stream stream);
+/* x = V[:, :k] y after the loop (k = report->iterations). */
+int pt_gmres_ws_finish(pt_gmres_ws *ws, int32_t k, double *x,
+                       pt_stream stream);
+
+/* ---- misc ----------------------------------------------------------------*/
+const char *pt_last_error(void);
+int32_t pt_abi_version(void);
+/* number of kernel launches issued by this library since load */
+int64_t pt_launch_count(void);
+/* algorithmic bytes of one A-apply / one n_it-sweep preconditioner apply
+ * (distinct kernels read once) */
+int64_t pt_bytes_apply_A(const pt_handle *h);
+int64_t pt_bytes_apply_M(const pt_handle *h, int32_t n_it);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PT_B200_H */

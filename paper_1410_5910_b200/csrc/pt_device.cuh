@@ -1,0 +1,91 @@
+// Device-side helpers shared by the executor and the GMRES kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pt_types.h"
+
+namespace pt {
+
+constexpr int EXEC_THREADS = 256;
+constexpr int EXEC_WARPS = EXEC_THREADS / 32;
+constexpr int DENSE_RPW = 2;  // rows per warp of a Y_DENSE task
+constexpr int DENSE_ROWS_PER_TASK = EXEC_WARPS * DENSE_RPW;
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// acc + a*b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+// acc + conj(a)*b
+__device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+  return acc;
+}
+
+// immutable operator data: read-only path, no L1 allocation (streamed once)
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+// vectors produced inside the launch by other CTAs: L2 only (L1 is not
+// coherent across SMs)
+__device__ __forceinline__ double2 ld_cg(const double2* p) { return __ldcg(p); }
+__device__ __forceinline__ void st_cg(double2* p, double2 v) { __stcg(p, v); }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+struct ExecArgs {
+  const DevTask* tasks;
+  const DevTerm* terms;
+  const DevEye* eyes;
+  const DevWait* waits;
+  int* ctr;   // counters; ctr[n_counters] is the queue head
+  int* head;
+  double2* slot[N_SLOTS];
+  const double2* dense;
+  const double2* fac;
+  const DevLeaf* leaves;
+  const DevSlot* slots;
+  const DevKernelPLR* kplr;
+  const int32_t* rowseg;
+  const DevSegment* segs;
+  const int32_t* seg_leaves;
+  int n_tasks;
+  int m;
+};
+
+__global__ void pt_exec_kernel(ExecArgs a);
+
+}  // namespace pt

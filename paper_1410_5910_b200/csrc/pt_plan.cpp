@@ -1,0 +1,522 @@
+// Host plan builder: turns the polarized entry table into task DAGs.
+//
+// Reference semantics restated here (file:line in pkg/src/helmsweep/):
+//  * A-apply  y_i = sum_j scale_ij K_ij x_j + eye_ij x_j
+//    (BlockInterfaceMatrix.matvec / BlockEntry.apply, trace_system.py:159-226)
+//  * split_DR (trace_system.py:499-524): row i goes to position inv[i] of the
+//    sweep permutation; down rows x down cols -> D_down, x up cols -> R_up,
+//    up rows x down cols -> R_down, x up cols -> D_up.
+//  * gs_sweep (solver.py:203-220) + solve_block_triangular
+//    (trace_system.py:527-548): x_p = sum_{j != p} D_pj x_j + (R u)_p - rhs_p,
+//    ascending for the down half, descending for the up half; a diagonal
+//    that is not exactly -I raises; entries on the not-yet-solved side
+//    multiply the zero-initialised x and contribute nothing.
+//
+// B200-specific restructuring (results equal up to rounding):
+//  * kernel terms of one block row that share a kernel and a scale are
+//    merged, K (x_a + x_b): in the A-apply this is K (x_down + x_up); in a
+//    sweep it is the D kernel applied to (x_new + u_old) of the R entry at
+//    the same block position, so every distinct kernel is streamed once per
+//    apply;
+//  * R-only terms of a sweep go to a pre-phase partial sum that does not
+//    wait for the sequential chain; the chain task starts from it;
+//  * sweep 1 starts from u = 0, so its R terms are skipped (bitwise exact).
+#include "pt_plan.h"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <set>
+#include <sstream>
+
+namespace pt {
+
+namespace {
+
+struct TermSpec {
+  int64_t kernel;
+  double s_re, s_im;
+  std::vector<VecRef> src;
+};
+struct EyeSpec {
+  double re, im;
+  VecRef src;
+};
+
+VecRef ref(int32_t slot, int64_t off) {
+  VecRef r;
+  r.slot = slot;
+  r.pad = 0;
+  r.off = off;
+  return r;
+}
+
+class Builder {
+ public:
+  Builder(const Operator& op, const PlanParams& pp) : op_(op), pp_(pp) {}
+
+  int emit_block(VecRef out, const std::vector<TermSpec>& terms,
+                 const std::vector<EyeSpec>& eyes, bool has_init, VecRef init,
+                 bool has_rhs, VecRef rhs, double rhs_coef) {
+    std::vector<int> waits;
+    for (const EyeSpec& e : eyes) add_wait(waits, e.src);
+    if (has_init) add_wait(waits, init);
+    if (has_rhs) add_wait(waits, rhs);
+    const int32_t term0 = (int32_t)prog_.terms.size();
+    const bool plr = op_.fmt == 1 && !terms.empty();
+    double ybytes = 0.0;
+    for (const TermSpec& t : terms) {
+      DevTerm dt{};
+      dt.kernel = (int32_t)t.kernel;
+      dt.nsrc = (int32_t)t.src.size();
+      dt.scale_re = t.s_re;
+      dt.scale_im = t.s_im;
+      for (size_t s = 0; s < t.src.size(); ++s) dt.src[s] = t.src[s];
+      dt.t_base = -1;
+      sweep_kernels_.insert(t.kernel);
+      prog_.term_bytes += op_.kernel_bytes[t.kernel];
+      if (plr) {
+        const int32_t ns = op_.nslot[t.kernel];
+        dt.t_base = alloc_t(ns);
+        // T tasks: t = Vt (sum of sources), warp per slot
+        std::vector<int> twaits;
+        for (const VecRef& s : t.src) add_wait(twaits, s);
+        const int g = new_group();
+        const int32_t term_idx = (int32_t)prog_.terms.size();
+        const DevKernelPLR& kp = op_.kplr[t.kernel];
+        for (int32_t s0 = 0; s0 < ns; s0 += pp_.plr_slots_per_task) {
+          DevTask tk{};
+          tk.type = TASK_T_PLR;
+          tk.r0 = s0;
+          tk.r1 = std::min<int32_t>(ns, s0 + pp_.plr_slots_per_task);
+          tk.term0 = term_idx;
+          tk.nterm = 1;
+          double c = 0;
+          for (int32_t s = tk.r0; s < tk.r1; ++s) c += 16.0 * op_.slots[kp.slot0 + s].cols;
+          push_task(tk, twaits, g, c);
+        }
+        register_producer(ref(SLOT_T, dt.t_base), g);
+        add_wait(waits, ref(SLOT_T, dt.t_base));
+        ybytes += 0.5 * (double)op_.kernel_bytes[t.kernel];
+      } else {
+        for (const VecRef& s : t.src) add_wait(waits, s);
+        ybytes += (double)op_.kernel_bytes[t.kernel];
+      }
+      prog_.terms.push_back(dt);
+    }
+    const int32_t eye0 = (int32_t)prog_.eyes.size();
+    for (const EyeSpec& e : eyes) {
+      DevEye de{};
+      de.re = e.re;
+      de.im = e.im;
+      de.src = e.src;
+      prog_.eyes.push_back(de);
+    }
+    const int g = new_group();
+    const int64_t m = op_.m;
+    const int rpt = plr ? pp_.plr_rows_per_task : pp_.dense_rows_per_task;
+    for (int64_t r0 = 0; r0 < m; r0 += rpt) {
+      DevTask tk{};
+      tk.type = plr ? TASK_Y_PLR : TASK_Y_DENSE;
+      tk.r0 = (int32_t)r0;
+      tk.r1 = (int32_t)std::min<int64_t>(m, r0 + rpt);
+      tk.term0 = term0;
+      tk.nterm = (int32_t)terms.size();
+      tk.eye0 = eye0;
+      tk.neye = (int32_t)eyes.size();
+      tk.out = out;
+      tk.has_init = has_init ? 1 : 0;
+      tk.init = init;
+      tk.has_rhs = has_rhs ? 1 : 0;
+      tk.rhs = rhs;
+      tk.rhs_coef = rhs_coef;
+      push_task(tk, waits, g, ybytes * double(tk.r1 - tk.r0) / double(m));
+    }
+    register_producer(out, g);
+    return g;
+  }
+
+  void begin_stage() { sweep_kernels_.clear(); }
+  void end_stage() {
+    for (int64_t k : sweep_kernels_) prog_.algo_bytes += op_.kernel_bytes[k];
+    sweep_kernels_.clear();
+  }
+
+  void need_slot(int32_t slot, int64_t elems) {
+    prog_.slot_elems[slot] = std::max(prog_.slot_elems[slot], elems);
+  }
+
+  Program finish() {
+    const int n = (int)prog_.tasks.size();
+    // depth = longest path from a root (topological levels)
+    std::vector<int> depth(n, 0), gdepth(groups_.size(), -1);
+    for (int t = 0; t < n; ++t) {
+      int d = 0;
+      for (int g : task_waits_[t]) d = std::max(d, gdepth[g] + 1);
+      depth[t] = d;
+      int& gd = gdepth[task_group_[t]];
+      gd = std::max(gd, d);
+    }
+    // bottom level = cost-weighted longest path to a sink
+    std::vector<double> bl(n, 0.0), gcons(groups_.size(), 0.0);
+    for (int t = n - 1; t >= 0; --t) {
+      bl[t] = task_cost_[t] + gcons[task_group_[t]];
+      for (int g : task_waits_[t]) gcons[g] = std::max(gcons[g], bl[t]);
+    }
+    std::vector<int> order(n);
+    for (int t = 0; t < n; ++t) order[t] = t;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      if (depth[a] != depth[b]) return depth[a] < depth[b];
+      return bl[a] > bl[b];
+    });
+    Program out;
+    out.terms = prog_.terms;
+    out.eyes = prog_.eyes;
+    out.t_elems = prog_.t_elems;
+    out.term_bytes = prog_.term_bytes;
+    out.algo_bytes = prog_.algo_bytes;
+    for (int s = 0; s < N_SLOTS; ++s) out.slot_elems[s] = prog_.slot_elems[s];
+    out.slot_elems[SLOT_T] = std::max<int64_t>(out.slot_elems[SLOT_T], prog_.t_elems);
+    out.n_counters = (int)groups_.size();
+    for (int idx : order) {
+      DevTask tk = prog_.tasks[idx];
+      tk.wait0 = (int32_t)out.waits.size();
+      tk.nwait = (int32_t)task_waits_[idx].size();
+      for (int g : task_waits_[idx]) {
+        DevWait w;
+        w.ctr = groups_[g].ctr;
+        w.val = groups_[g].count;
+        out.waits.push_back(w);
+      }
+      out.tasks.push_back(tk);
+    }
+    return out;
+  }
+
+ private:
+  struct Group {
+    int ctr;
+    int count;
+  };
+
+  int new_group() {
+    Group g;
+    g.ctr = (int)groups_.size();
+    g.count = 0;
+    groups_.push_back(g);
+    return g.ctr;
+  }
+
+  void register_producer(VecRef block, int g) {
+    producer_[std::make_pair(block.slot, block.off)] = g;
+  }
+
+  void add_wait(std::vector<int>& waits, VecRef r) {
+    auto it = producer_.find(std::make_pair(r.slot, r.off));
+    if (it == producer_.end()) return;
+    if (std::find(waits.begin(), waits.end(), it->second) == waits.end())
+      waits.push_back(it->second);
+  }
+
+  int64_t alloc_t(int64_t n) {
+    const int64_t base = prog_.t_elems;
+    prog_.t_elems += (n + 7) / 8 * 8;
+    return base;
+  }
+
+  void push_task(DevTask tk, const std::vector<int>& waits, int g, double cost) {
+    tk.signal = groups_[g].ctr;
+    groups_[g].count += 1;
+    prog_.tasks.push_back(tk);
+    task_waits_.push_back(waits);
+    task_group_.push_back(g);
+    task_cost_.push_back(cost);
+  }
+
+  const Operator& op_;
+  PlanParams pp_;
+  Program prog_;
+  std::map<std::pair<int32_t, int64_t>, int> producer_;
+  std::vector<Group> groups_;
+  std::vector<std::vector<int>> task_waits_;
+  std::vector<int> task_group_;
+  std::vector<double> task_cost_;
+  std::set<int64_t> sweep_kernels_;
+};
+
+bool same_scale(const TermSpec& t, const HostEntry& e) {
+  return t.kernel == e.kernel && t.s_re == e.s_re && t.s_im == e.s_im;
+}
+
+// A-apply: one output block per natural block row.
+void emit_A(Builder& b, const Operator& op, int32_t in_slot, int32_t out_slot) {
+  const int64_t m = op.m;
+  b.begin_stage();
+  b.need_slot(out_slot, op.nb * m);
+  size_t k = 0;
+  for (int64_t i = 0; i < op.nb; ++i) {
+    std::vector<TermSpec> terms;
+    std::vector<EyeSpec> eyes;
+    for (; k < op.entries.size() && op.entries[k].row == i; ++k) {
+      const HostEntry& e = op.entries[k];
+      const VecRef src = ref(in_slot, e.col * m);
+      if (e.kernel >= 0) {
+        bool merged = false;
+        for (TermSpec& t : terms) {
+          if (same_scale(t, e) && t.src.size() < 2) {
+            t.src.push_back(src);
+            merged = true;
+            break;
+          }
+        }
+        if (!merged) terms.push_back(TermSpec{e.kernel, e.s_re, e.s_im, {src}});
+      }
+      if (e.e_re != 0.0 || e.e_im != 0.0) eyes.push_back(EyeSpec{e.e_re, e.e_im, src});
+    }
+    b.emit_block(ref(out_slot, i * m), terms, eyes, false, VecRef{}, false, VecRef{}, 0.0);
+  }
+  b.end_stage();
+}
+
+struct HalfEntry {
+  const HostEntry* e;
+  int64_t jj;  // block column within its half
+  bool is_d;
+};
+
+// One Gauss-Seidel sweep u_new = D^-1 (P rhs - R u_old).
+void emit_sweep(Builder& b, const Operator& op, VecRef rhs, bool has_uold, VecRef uold,
+                VecRef unew, VecRef pre) {
+  const int64_t m = op.m, nt = op.nt;
+  b.begin_stage();
+  b.need_slot(unew.slot, unew.off + op.nb * m);
+  b.need_slot(pre.slot, pre.off + op.nb * m);
+  // rows[h][p]: entries of half-row p
+  std::vector<std::vector<HalfEntry>> rows[2];
+  rows[0].resize(nt);
+  rows[1].resize(nt);
+  for (const HostEntry& e : op.entries) {
+    const int64_t pos = op.inv[e.row];
+    const int h = pos >= nt ? 1 : 0;
+    const int64_t p = pos - h * nt;
+    const int colhalf = e.col >= nt ? 1 : 0;
+    rows[h][p].push_back(HalfEntry{&e, e.col - colhalf * nt, colhalf == h});
+  }
+  auto unew_ref = [&](int h, int64_t j) { return ref(unew.slot, unew.off + (h * nt + j) * m); };
+  auto uold_ref = [&](int h, int64_t j) {
+    return ref(uold.slot, uold.off + ((1 - h) * nt + j) * m);
+  };
+  // levels
+  std::vector<int> level[2];
+  for (int h = 0; h < 2; ++h) {
+    level[h].assign(nt, 0);
+    for (int64_t q = 0; q < nt; ++q) {
+      const int64_t p = h == 0 ? q : nt - 1 - q;
+      int lv = 0;
+      for (const HalfEntry& he : rows[h][p]) {
+        if (!he.is_d) continue;
+        const bool chain = h == 0 ? he.jj < p : he.jj > p;
+        if (chain) lv = std::max(lv, level[h][he.jj] + 1);
+      }
+      level[h][p] = lv;
+    }
+  }
+  int max_level = 0;
+  for (int h = 0; h < 2; ++h)
+    for (int v : level[h]) max_level = std::max(max_level, v);
+
+  struct RowPlan {
+    std::vector<TermSpec> chain_terms, r_terms;
+    std::vector<EyeSpec> chain_eyes, r_eyes;
+  };
+  std::vector<RowPlan> plans[2];
+  for (int h = 0; h < 2; ++h) {
+    plans[h].resize(nt);
+    for (int64_t p = 0; p < nt; ++p) {
+      RowPlan& rp = plans[h][p];
+      std::vector<TermSpec> rk;
+      for (const HalfEntry& he : rows[h][p]) {
+        const HostEntry& e = *he.e;
+        if (he.is_d) {
+          if (he.jj == p) continue;  // diagonal: validated -I (see validate)
+          const bool chain = h == 0 ? he.jj < p : he.jj > p;
+          if (!chain) continue;  // multiplies the zero-initialised x
+          const VecRef src = unew_ref(h, he.jj);
+          if (e.kernel >= 0) rp.chain_terms.push_back(TermSpec{e.kernel, e.s_re, e.s_im, {src}});
+          if (e.e_re != 0.0 || e.e_im != 0.0) rp.chain_eyes.push_back(EyeSpec{e.e_re, e.e_im, src});
+        } else if (has_uold) {
+          const VecRef src = uold_ref(h, he.jj);
+          if (e.kernel >= 0) rk.push_back(TermSpec{e.kernel, e.s_re, e.s_im, {src}});
+          if (e.e_re != 0.0 || e.e_im != 0.0) rp.r_eyes.push_back(EyeSpec{e.e_re, e.e_im, src});
+        }
+      }
+      // merge R kernel terms into chain terms with the same kernel and scale
+      for (TermSpec& r : rk) {
+        bool merged = false;
+        for (TermSpec& c : rp.chain_terms) {
+          if (c.kernel == r.kernel && c.s_re == r.s_re && c.s_im == r.s_im && c.src.size() == 1) {
+            c.src.push_back(r.src[0]);
+            merged = true;
+            break;
+          }
+        }
+        if (!merged) rp.r_terms.push_back(r);
+      }
+    }
+  }
+  // pre-phase: R-only terms - rhs, for rows that also have chain work
+  std::vector<bool> has_pre[2];
+  for (int h = 0; h < 2; ++h) {
+    has_pre[h].assign(nt, false);
+    for (int64_t p = 0; p < nt; ++p) {
+      RowPlan& rp = plans[h][p];
+      const bool chain = !rp.chain_terms.empty() || !rp.chain_eyes.empty();
+      const bool ronly = !rp.r_terms.empty() || !rp.r_eyes.empty();
+      if (chain && ronly) {
+        has_pre[h][p] = true;
+        const VecRef dst = ref(pre.slot, pre.off + (h * nt + p) * m);
+        b.emit_block(dst, rp.r_terms, rp.r_eyes, false, VecRef{}, true,
+                     ref(rhs.slot, rhs.off + op.perm[h * nt + p] * m), -1.0);
+      }
+    }
+  }
+  // chain, level by level, both halves interleaved
+  for (int lv = 0; lv <= max_level; ++lv) {
+    for (int h = 0; h < 2; ++h) {
+      for (int64_t q = 0; q < nt; ++q) {
+        const int64_t p = h == 0 ? q : nt - 1 - q;
+        if (level[h][p] != lv) continue;
+        RowPlan& rp = plans[h][p];
+        const VecRef rhs_p = ref(rhs.slot, rhs.off + op.perm[h * nt + p] * m);
+        if (has_pre[h][p]) {
+          b.emit_block(unew_ref(h, p), rp.chain_terms, rp.chain_eyes, true,
+                       ref(pre.slot, pre.off + (h * nt + p) * m), false, VecRef{}, 0.0);
+        } else {
+          std::vector<TermSpec> terms = rp.chain_terms;
+          terms.insert(terms.end(), rp.r_terms.begin(), rp.r_terms.end());
+          std::vector<EyeSpec> eyes = rp.chain_eyes;
+          eyes.insert(eyes.end(), rp.r_eyes.begin(), rp.r_eyes.end());
+          b.emit_block(unew_ref(h, p), terms, eyes, false, VecRef{}, true, rhs_p, -1.0);
+        }
+      }
+    }
+  }
+  b.end_stage();
+}
+
+void emit_M(Builder& b, const Operator& op, int n_it, VecRef rhs) {
+  const int64_t N = op.nb * op.m;
+  bool has_old = false;
+  VecRef uold{};
+  for (int k = 0; k < n_it; ++k) {
+    const VecRef out = (k == n_it - 1) ? ref(SLOT_OUT, 0) : ref(SLOT_U1, (int64_t)k * N);
+    emit_sweep(b, op, rhs, has_old, uold, out, ref(SLOT_PRE, (int64_t)k * N));
+    uold = out;
+    has_old = true;
+  }
+}
+
+}  // namespace
+
+bool validate_operator(Operator& op, std::string& err) {
+  std::ostringstream os;
+  if (op.m <= 0) {
+    err = "block size m must be positive";
+    return false;
+  }
+  if (op.nb <= 0 || op.nb % 2) {
+    err = "polarized matrix must be square with an even block count";
+    return false;
+  }
+  op.nt = op.nb / 2;
+  if ((int64_t)op.perm.size() != op.nb) {
+    err = "sweep permutation has the wrong length";
+    return false;
+  }
+  op.inv.assign(op.nb, -1);
+  for (int64_t p = 0; p < op.nb; ++p) {
+    const int64_t v = op.perm[p];
+    if (v < 0 || v >= op.nb || op.inv[v] != -1) {
+      err = "sweep permutation is not a permutation of the block rows";
+      return false;
+    }
+    op.inv[v] = p;
+  }
+  std::sort(op.entries.begin(), op.entries.end(), [](const HostEntry& a, const HostEntry& b) {
+    return a.row != b.row ? a.row < b.row : a.col < b.col;
+  });
+  for (size_t i = 0; i < op.entries.size(); ++i) {
+    const HostEntry& e = op.entries[i];
+    if (e.row < 0 || e.row >= op.nb || e.col < 0 || e.col >= op.nb) {
+      os << "block (" << e.row << "," << e.col << ") outside " << op.nb << "x" << op.nb;
+      err = os.str();
+      return false;
+    }
+    if (i && op.entries[i - 1].row == e.row && op.entries[i - 1].col == e.col) {
+      os << "block (" << e.row << "," << e.col << ") assigned twice";
+      err = os.str();
+      return false;
+    }
+    if (e.kernel < -1 || e.kernel >= op.nk) {
+      os << "block (" << e.row << "," << e.col << ") references kernel " << e.kernel;
+      err = os.str();
+      return false;
+    }
+  }
+  return true;
+}
+
+// A diagonal block of D that is not exactly -I makes the sweep raise
+// (trace_system.py:542-544); returns the message or "".
+std::string sweep_diagonal_error(const Operator& op) {
+  for (const HostEntry& e : op.entries) {
+    const int64_t pos = op.inv[e.row];
+    const int h = pos >= op.nt ? 1 : 0;
+    const int colhalf = e.col >= op.nt ? 1 : 0;
+    if (colhalf != h) continue;
+    const int64_t p = pos - h * op.nt, jj = e.col - colhalf * op.nt;
+    if (jj == p && !(e.kernel < 0 && e.e_re == -1.0 && e.e_im == 0.0)) {
+      std::ostringstream os;
+      os << "diagonal block " << p << " is not exactly -I";
+      return os.str();
+    }
+  }
+  return "";
+}
+
+Program build_apply_A(const Operator& op, const PlanParams& pp) {
+  Builder b(op, pp);
+  emit_A(b, op, SLOT_IN, SLOT_OUT);
+  return b.finish();
+}
+
+Program build_apply_M(const Operator& op, int n_it, const PlanParams& pp) {
+  Builder b(op, pp);
+  emit_M(b, op, n_it, ref(SLOT_IN, 0));
+  return b.finish();
+}
+
+Program build_gs_sweep(const Operator& op, const PlanParams& pp) {
+  Builder b(op, pp);
+  emit_sweep(b, op, ref(SLOT_IN, 0), true, ref(SLOT_AUX, 0), ref(SLOT_OUT, 0), ref(SLOT_PRE, 0));
+  return b.finish();
+}
+
+Program build_A_then_M(const Operator& op, int n_it, const PlanParams& pp) {
+  Builder b(op, pp);
+  emit_A(b, op, SLOT_IN, SLOT_Y);
+  emit_M(b, op, n_it, ref(SLOT_Y, 0));
+  return b.finish();
+}
+
+std::string Program::describe() const {
+  std::ostringstream os;
+  int counts[3] = {0, 0, 0};
+  for (const DevTask& t : tasks) counts[t.type]++;
+  os << tasks.size() << " tasks (Ydense " << counts[0] << ", Yplr " << counts[1] << ", Tplr "
+     << counts[2] << "), " << terms.size() << " terms, " << n_counters << " counters, algo "
+     << algo_bytes << " B, streamed " << term_bytes << " B";
+  return os.str();
+}
+
+}  // namespace pt

@@ -1,0 +1,101 @@
+// Plain-old-data structures shared by the host plan builder (pt_plan.cpp)
+// and the device executor (pt_exec.cu).
+//
+// A "program" is a DAG of tasks over interface vectors.  Every task writes
+// a disjoint piece of one vector (rows of one m-block, or a slot range of a
+// PLR t-buffer) and is computed entirely by one CTA in a fixed summation
+// order, so results are bitwise repeatable no matter which CTA runs it
+// (the reference pins bitwise-repeatable applies, test_solver.py:93-117).
+// Dependencies are counters: a producer group of n tasks bumps its counter
+// n times; consumers wait for the count.
+#pragma once
+#include <stdint.h>
+
+namespace pt {
+
+// vector slots of a program launch (base pointers supplied per launch)
+enum Slot : int32_t {
+  SLOT_IN = 0,    // program input vector (x, r, rhs ...)
+  SLOT_OUT = 1,   // program output vector
+  SLOT_Y = 2,     // A-apply result inside an A->M program
+  SLOT_U1 = 3,    // sweep iterates
+  SLOT_U2 = 4,
+  SLOT_PRE = 5,   // pre-phase partial sums of the sweeps
+  SLOT_T = 6,     // PLR t = Vt x buffers (one region per term instance)
+  SLOT_AUX = 7,   // second input (u_in of gs_sweep)
+  N_SLOTS = 8
+};
+
+enum TaskType : int32_t {
+  TASK_Y_DENSE = 0,  // rows of an output block from dense kernel terms
+  TASK_Y_PLR = 1,    // rows of an output block from PLR terms (U t)
+  TASK_T_PLR = 2,    // t = Vt (sum of sources) for a slot range of a term
+};
+
+struct VecRef {
+  int32_t slot;
+  int32_t pad;
+  int64_t off;  // complex-element offset into the slot vector
+};
+
+// one kernel term: scale * K (src0 [+ src1])
+struct DevTerm {
+  int32_t kernel;
+  int32_t nsrc;
+  double scale_re, scale_im;
+  VecRef src[2];
+  int64_t t_base;  // PLR: offset of this term instance's t in SLOT_T
+};
+
+// one identity term: coef * v
+struct DevEye {
+  double re, im;
+  VecRef src;
+};
+
+struct DevWait {
+  int32_t ctr;
+  int32_t val;
+};
+
+struct DevTask {
+  int32_t type;
+  int32_t r0, r1;      // rows [r0,r1) of the block (Y) or slots (T)
+  int32_t term0, nterm;  // Y: term range; T: term0 = the term instance
+  int32_t eye0, neye;
+  int32_t wait0, nwait;
+  int32_t signal;      // counter to bump when done (-1: none)
+  int32_t has_init;
+  int32_t has_rhs;
+  VecRef out;          // Y: output block start
+  VecRef init;         // Y: partial sum to start from
+  VecRef rhs;          // Y: + rhs_coef * rhs
+  double rhs_coef;
+};
+
+// PLR storage on the device.  For each leaf the factors are stored as
+// rank "slots": slot c holds U[:, c] (rows contiguous, i.e. U column-major)
+// and Vt[c, :] (cols contiguous).
+struct DevLeaf {
+  int64_t u_off;   // complex offset of U column 0 (column-major rows x rank)
+  int64_t v_off;   // complex offset of Vt row 0 (row-major rank x cols)
+  int32_t row_off, col_off, rows, cols, rank, slot0;  // slot0 within kernel
+};
+
+struct DevSlot {     // one Vt row, for the t-phase
+  int64_t v_off;     // complex offset of this Vt row
+  int32_t col_off, cols;
+};
+
+struct DevKernelPLR {
+  int32_t leaf0, nleaf;      // into the leaf table
+  int32_t slot0, nslot;      // into the slot table (nslot = sum of ranks)
+  int32_t seg0;              // row -> segment map at rowseg[seg0 + row]
+  int32_t pad;
+};
+
+struct DevSegment {          // a row band covered by a fixed leaf set
+  int32_t leaf_list0, nleaf; // into seg_leaves
+};
+
+}  // namespace pt

@@ -1,0 +1,243 @@
+"""Device-resident polarized interface operator (the uploaded offline state).
+
+``DeviceOperator`` owns one ``pt_handle`` of libpt_b200.so: the entry table
+of the polarized "jump" system (trace_system.py:368-472), the sweep
+permutation (:353-365) and the kernels (dense Green's blocks or PLR leaves)
+uploaded once to HBM.  Its methods are the device versions of the
+reference's online operators:
+
+=======================  ===============================================
+``apply_A``              ``BlockInterfaceMatrix.matvec`` (:219-226)
+``apply_M``              ``preconditioner_apply`` (solver.py:223-228)
+``gs_sweep``             ``gs_sweep`` (solver.py:203-220)
+``gmres``                ``gmres_solve`` (solver.py:231-295) on the device
+=======================  ===============================================
+
+Vectors may be numpy arrays (copied to and from the device) or torch
+complex128 CUDA tensors (used in place, stream-ordered on the current
+torch stream).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as nat
+from .cache import read_case
+
+__all__ = ["DeviceOperator", "load_case_arrays"]
+
+_ENTRY_DT = np.dtype([("row", "<i8"), ("col", "<i8"), ("kernel", "<i8"),
+                      ("scale_re", "<f8"), ("scale_im", "<f8"),
+                      ("eye_re", "<f8"), ("eye_im", "<f8")])
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def load_case_arrays(path):
+    """(meta, arrays) of a PTC1 case; resolves ``operator_case`` links."""
+    path = Path(path)
+    meta, arrays = read_case(path)
+    link = meta.get("operator_case")
+    if link:
+        ometa, oarr = read_case(path.with_name(f"{link}.ptc"))
+        for k in ("entries", "coefs", "perm", "dense", "leaves", "factors", "kernel_bytes"):
+            if k in oarr:
+                arrays[k] = oarr[k]
+        for k in ("kernel_format", "n_kernels", "kernel_bytes"):
+            meta[k] = ometa[k]
+    return meta, arrays
+
+
+class DeviceOperator:
+    def __init__(self, *, m, n_block_rows, entries, coefs, perm, dense=None, leaves=None,
+                 factors=None, device=None):
+        torch = _torch()
+        lib = nat.lib()
+        if not torch.cuda.is_available():
+            raise RuntimeError("DeviceOperator needs a CUDA device (no CPU fallback)")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.m = int(m)
+        self.n_block_rows = int(n_block_rows)
+        self.N = self.m * self.n_block_rows
+        self.nt = self.n_block_rows // 2
+        entries = np.asarray(entries, dtype=np.int64).reshape(-1, 3)
+        coefs = np.asarray(coefs, dtype=np.complex128).reshape(-1, 2)
+        ent = np.zeros(entries.shape[0], dtype=_ENTRY_DT)
+        ent["row"], ent["col"], ent["kernel"] = entries[:, 0], entries[:, 1], entries[:, 2]
+        ent["scale_re"], ent["scale_im"] = coefs[:, 0].real, coefs[:, 0].imag
+        ent["eye_re"], ent["eye_im"] = coefs[:, 1].real, coefs[:, 1].imag
+        self.perm = np.ascontiguousarray(np.asarray(perm, dtype=np.int64))
+        self.entries = entries
+        self.coefs = coefs
+        lay = nat.Layout()
+        lay.m = self.m
+        lay.n_block_rows = self.n_block_rows
+        if dense is not None:
+            dense = np.ascontiguousarray(dense, dtype=np.complex128)
+            lay.kernel_format = nat.PT_KERNEL_DENSE
+            lay.n_kernels = dense.shape[0]
+            self.kernel_format = "dense"
+            dptr, lptr, nleaf, fptr, nfac = dense.ctypes.data, None, 0, None, 0
+        else:
+            leaves = np.ascontiguousarray(np.asarray(leaves, dtype=np.int64).reshape(-1, 8))
+            factors = np.ascontiguousarray(factors, dtype=np.complex128)
+            lay.kernel_format = nat.PT_KERNEL_PLR
+            kmax = int(entries[:, 2].max()) + 1 if entries.size else 0
+            lay.n_kernels = max(kmax, int(leaves[:, 0].max()) + 1 if leaves.size else 0)
+            self.kernel_format = "plr"
+            dptr = None
+            lptr = leaves.ctypes.data_as(C.POINTER(nat.Leaf))
+            nleaf = leaves.shape[0]
+            fptr = factors.ctypes.data
+            nfac = factors.shape[0]
+        self.n_kernels = lay.n_kernels
+        h = C.c_void_p()
+        rc = lib.pt_create(C.byref(lay), ent.ctypes.data_as(C.POINTER(nat.Entry)), ent.shape[0],
+                           self.perm.ctypes.data_as(C.POINTER(C.c_int64)), dptr, lptr, nleaf,
+                           fptr, nfac, self.device, C.byref(h))
+        nat.check(rc, "pt_create")
+        self._h = h
+
+    # ------------------------------------------------------------------
+    @classmethod
+    def from_case(cls, path, device=None):
+        meta, arr = load_case_arrays(path)
+        op = cls.from_arrays(meta, arr, device=device)
+        op.meta = meta
+        return op
+
+    @classmethod
+    def from_arrays(cls, meta, arr, device=None):
+        n_block_rows = int(meta.get("n_block_rows", 2 * meta.get("nt", 0)))
+        kw = dict(m=meta["m"], n_block_rows=n_block_rows, entries=arr["entries"],
+                  coefs=arr["coefs"], perm=arr["perm"], device=device)
+        if "dense" in arr:
+            kw["dense"] = arr["dense"]
+        else:
+            kw["leaves"], kw["factors"] = arr["leaves"], arr["factors"]
+        return cls(**kw)
+
+    @classmethod
+    def from_reference(cls, pol, perm, device=None):
+        """Upload a reference ``state.pol`` / ``state.perm`` pair."""
+        from .capture import capture_operator
+        meta, arr = capture_operator(pol, perm)
+        return cls.from_arrays(meta, arr, device=device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            nat.lib().pt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    @property
+    def handle(self):
+        return self._h
+
+    def stream(self):
+        return C.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def _dev_vec(self, x, name="vector"):
+        """(tensor on device, was_numpy)."""
+        torch = _torch()
+        if isinstance(x, torch.Tensor):
+            if x.dtype != torch.complex128 or x.device.type != "cuda" or x.device.index != self.device:
+                raise ValueError(f"{name} must be a complex128 tensor on cuda:{self.device}")
+            if x.shape != (self.N,):
+                raise ValueError(f"polarized vector has length {tuple(x.shape)}, expected {self.N}")
+            return x.contiguous(), False
+        a = np.asarray(x, dtype=np.complex128)
+        if a.shape != (self.N,):
+            raise ValueError(f"polarized vector has length {a.shape[0] if a.ndim else a.shape}, "
+                             f"expected {self.N}")
+        return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}"), True
+
+    def _out(self, out, host):
+        torch = _torch()
+        if out is None:
+            return torch.empty(self.N, dtype=torch.complex128, device=f"cuda:{self.device}")
+        if host:
+            raise ValueError("out= is only supported for CUDA tensor inputs")
+        return out
+
+    @staticmethod
+    def _ret(t, host):
+        return t.cpu().numpy() if host else t
+
+    def apply_A(self, x, out=None):
+        xd, host = self._dev_vec(x)
+        y = self._out(out, host)
+        nat.check(nat.lib().pt_apply_A(self._h, xd.data_ptr(), y.data_ptr(), self.stream()),
+                  "pt_apply_A")
+        return self._ret(y, host)
+
+    def apply_M(self, r, n_it=2, out=None):
+        rd, host = self._dev_vec(r)
+        z = self._out(out, host)
+        nat.check(nat.lib().pt_apply_M(self._h, rd.data_ptr(), z.data_ptr(), int(n_it),
+                                       self.stream()), "pt_apply_M")
+        return self._ret(z, host)
+
+    def gs_sweep(self, rhs, u_in, out=None):
+        rd, host = self._dev_vec(rhs, "rhs")
+        ud, _ = self._dev_vec(u_in, "u_in")
+        z = self._out(out, host)
+        nat.check(nat.lib().pt_gs_sweep(self._h, rd.data_ptr(), ud.data_ptr(), z.data_ptr(),
+                                        self.stream()), "pt_gs_sweep")
+        return self._ret(z, host)
+
+    def gmres(self, b, rel_tol=1e-7, max_iter=100, n_it=2, out=None):
+        """Device GMRES; returns (x, report dict).  One host sync per iteration."""
+        bd, host = self._dev_vec(b, "b")
+        x = self._out(out, host)
+        cfg = nat.GmresConfigC(float(rel_tol), int(max_iter), int(n_it))
+        hist = (C.c_double * int(max_iter))()
+        rep = nat.Report()
+        rep.residual_history = C.cast(hist, C.POINTER(C.c_double))
+        rc = nat.lib().pt_gmres(self._h, bd.data_ptr(), x.data_ptr(), C.byref(cfg), C.byref(rep),
+                                self.stream())
+        nat.check(rc, "pt_gmres")
+        return self._ret(x, host), _report_dict(rep, hist)
+
+    def gmres_host(self, b_host, x_host, rel_tol=1e-7, max_iter=100, n_it=2):
+        """GMRES from HOST buffers (pinned torch tensors or numpy): H2D, solve, D2H."""
+        cfg = nat.GmresConfigC(float(rel_tol), int(max_iter), int(n_it))
+        hist = (C.c_double * int(max_iter))()
+        rep = nat.Report()
+        rep.residual_history = C.cast(hist, C.POINTER(C.c_double))
+        bp = b_host.data_ptr() if hasattr(b_host, "data_ptr") else b_host.ctypes.data
+        xp = x_host.data_ptr() if hasattr(x_host, "data_ptr") else x_host.ctypes.data
+        rc = nat.lib().pt_gmres_host(self._h, bp, xp, C.byref(cfg), C.byref(rep), self.stream())
+        nat.check(rc, "pt_gmres_host")
+        return _report_dict(rep, hist)
+
+    def bytes_apply_A(self):
+        return int(nat.lib().pt_bytes_apply_A(self._h))
+
+    def bytes_apply_M(self, n_it=2):
+        return int(nat.lib().pt_bytes_apply_M(self._h, int(n_it)))
+
+
+def _report_dict(rep, hist):
+    k = int(rep.iterations)
+    return {
+        "iterations": k,
+        "flag": nat.FLAGS.get(int(rep.flag), "unknown"),
+        "converged": bool(rep.converged),
+        "true_residual": float(rep.true_residual),
+        "beta": float(rep.beta),
+        "residual_history": [float(hist[i]) for i in range(k)],
+    }

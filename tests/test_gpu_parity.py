@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's vectors.
+
+Bars (BASELINE.json north_star): every operator apply within 1e-12 relative
+L2 of the reference; GMRES iteration count within +-1; interface traces
+within 1e-8 relative L2.  Applies are also checked for bitwise
+repeatability and linearity (test_solver.py:93-117).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import FIXTURES, case_path, golden_path
+from oracle import ref_port as O
+from paper_1410_5910_b200.operator import DeviceOperator, load_case_arrays
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-12
+TRACE_TOL = 1e-8
+
+_OPS = {}
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def get(name, big=False):
+    path = case_path(name) if big else golden_path(name)
+    if not path.exists():
+        pytest.skip(f"{path} not generated")
+    if name not in _OPS:
+        meta, arr = load_case_arrays(path)
+        _OPS[name] = (meta, arr, DeviceOperator.from_arrays(meta, arr))
+    return _OPS[name]
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_apply_A(cuda_ok, name):
+    meta, arr, op = get(name)
+    assert rel(op.apply_A(arr["probe_x"]), arr["probe_Ax"]) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_apply_M(cuda_ok, name):
+    meta, arr, op = get(name)
+    assert rel(op.apply_M(arr["probe_x"], n_it=2), arr["probe_Mx"]) <= APPLY_TOL
+    assert rel(op.apply_M(arr["probe_x"], n_it=1), arr["probe_M1x"]) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_gs_sweep(cuda_ok, name):
+    meta, arr, op = get(name)
+    assert rel(op.gs_sweep(arr["probe_x"], arr["probe_u"]), arr["probe_sweep"]) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_applies_bitwise_repeatable_and_linear(cuda_ok, name):
+    import torch
+    meta, arr, op = get(name)
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(op.N) + 1j * rng.standard_normal(op.N)
+    y = rng.standard_normal(op.N) + 1j * rng.standard_normal(op.N)
+    xd = torch.from_numpy(x).cuda()
+    assert torch.equal(op.apply_A(xd), op.apply_A(xd))
+    assert torch.equal(op.apply_M(xd), op.apply_M(xd))
+    a, b = 0.3 - 1.1j, -2.0 + 0.4j
+    combo = op.apply_M(a * x + b * y)
+    split = a * op.apply_M(x) + b * op.apply_M(y)
+    assert np.abs(combo - split).max() <= 1e-13 * np.abs(combo).max()
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_gmres_matches_reference(cuda_ok, name):
+    meta, arr, op = get(name)
+    ref = meta["solves"][0]
+    x, rep = op.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"], max_iter=100, n_it=2)
+    assert abs(rep["iterations"] - ref["iterations"]) <= 1
+    assert rep["converged"] == ref["converged"]
+    nt, m = meta["nt"], meta["m"]
+    assert rel(x[: nt * m] + x[nt * m:], arr["ref_traces"][0]) <= TRACE_TOL
+    assert rel(x, arr["ref_x"][0]) <= TRACE_TOL
+    assert rep["true_residual"] <= 10 * meta["gmres_tol"]
+    hist = np.asarray(arr["ref_hist"][0][: ref["iterations"]])
+    k = min(len(hist), rep["iterations"])
+    assert np.allclose(rep["residual_history"][:k], hist[:k], rtol=1e-4, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", FIXTURES[:2])
+def test_gmres_bitwise_repeatable(cuda_ok, name):
+    meta, arr, op = get(name)
+    x1, r1 = op.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"])
+    x2, r2 = op.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"])
+    assert np.array_equal(x1, x2) and r1 == r2
+
+
+def test_reference_api_path(cuda_ok):
+    from paper_1410_5910_b200 import solver as S
+    state = S.OfflineState.from_case(golden_path("fx_tiny"))
+    meta, arr = load_case_arrays(golden_path("fx_tiny"))
+    cfg = S.PreconditionerConfig()
+    z = S.preconditioner_apply(cfg, state.d, state.r, state.perm, arr["probe_x"])
+    assert rel(z, arr["probe_Mx"]) <= APPLY_TOL
+    u = S.gs_sweep(state.d, state.r, state.perm, arr["probe_x"], arr["probe_u"])
+    assert rel(u, arr["probe_sweep"]) <= APPLY_TOL
+    assert rel(state.pol.matvec(arr["probe_x"]), arr["probe_Ax"]) <= APPLY_TOL
+    x, rep = S.solve_online(state, arr["rhs"][0], gmres=S.GmresConfig(rel_tol=meta["gmres_tol"]))
+    assert rel(rep.traces, arr["ref_traces"][0]) <= TRACE_TOL
+    zero_x, zrep = S.solve_online(state, np.zeros(state.op.N, complex))
+    assert zrep.converged and zrep.iterations == 0 and np.all(zero_x == 0)
+    with pytest.raises(ValueError, match="variant"):
+        S.solve_online(state, arr["rhs"][0], precond=S.PreconditionerConfig(variant="extrapolation"))
+
+
+# ---- the reference's GMRES unit tests through the device Arnoldi/Givens path
+
+
+def _gm(apply_A, b, cfg=None, M=lambda v: v):
+    from paper_1410_5910_b200 import solver as S
+    return S.gmres_solve(apply_A, M, b, cfg or S.GmresConfig())
+
+
+def test_gpu_gmres_identity_breakdown(cuda_ok):
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(20) + 1j * rng.standard_normal(20)
+    x, rep = _gm(lambda v: v, b)
+    assert rep.converged and rep.flag == "breakdown" and rep.iterations == 1
+    assert np.abs(x - b).max() <= 1e-13 * np.abs(b).max()
+    assert rep.true_residual <= 1e-13
+
+
+def test_gpu_gmres_dense_3x3(cuda_ok):
+    from paper_1410_5910_b200 import solver as S
+    a = np.array([[4.0, 1.0, 0.0], [1.0, 3.0, 1.0], [0.0, 1.0, 2.0]]) + 0.5j * np.eye(3)
+    b = np.array([1.0, -2.0, 0.5]) + 1j * np.array([0.0, 1.0, -0.5])
+    x, rep = _gm(lambda v: a @ v, b, S.GmresConfig(rel_tol=1e-12))
+    assert rep.converged and rep.iterations <= 3
+    expect = np.linalg.solve(a, b)
+    assert np.abs(x - expect).max() <= 1e-12 * np.abs(expect).max()
+    h = rep.residual_history
+    assert all(h[i + 1] <= h[i] * (1 + 1e-12) + 1e-15 for i in range(len(h) - 1))
+
+
+def test_gpu_gmres_torch_callables(cuda_ok):
+    import torch
+    from paper_1410_5910_b200 import solver as S
+    a = torch.tensor([[4.0, 1.0, 0.0], [1.0, 3.0, 1.0], [0.0, 1.0, 2.0]], dtype=torch.complex128,
+                     device="cuda") + 0.5j * torch.eye(3, dtype=torch.complex128, device="cuda")
+    b = torch.tensor([1.0 + 0j, -2.0 + 1j, 0.5 - 0.5j], dtype=torch.complex128, device="cuda")
+    x, rep = S.gmres_solve(lambda v: a @ v, lambda v: v, b, S.GmresConfig(rel_tol=1e-12))
+    assert isinstance(x, torch.Tensor) and rep.converged
+    assert torch.allclose(a @ x, b, rtol=0, atol=1e-11)
+
+
+def test_gpu_gmres_zero_rhs(cuda_ok):
+    x, rep = _gm(lambda v: v, np.zeros(5, complex))
+    assert rep.converged and rep.iterations == 0 and np.all(x == 0)
+
+
+def test_gpu_gmres_stagnation(cuda_ok):
+    from paper_1410_5910_b200 import solver as S
+    x, rep = _gm(lambda v: np.roll(v, 1), np.eye(50, dtype=complex)[:, 0],
+                 S.GmresConfig(rel_tol=1e-12, max_iter=40))
+    assert rep.flag == "stagnation" and not rep.converged
+    assert len(rep.residual_history) >= 11
+
+
+def test_gpu_gmres_nan_aborts(cuda_ok):
+    with pytest.raises(RuntimeError, match="non-finite"):
+        _gm(lambda v: np.full_like(v, np.nan), np.ones(4, complex))
+
+
+def test_gpu_gmres_maxiter(cuda_ok):
+    from paper_1410_5910_b200 import solver as S
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((30, 30)) + 1j * rng.standard_normal((30, 30))
+    b = rng.standard_normal(30) + 0j
+    x, rep = _gm(lambda v: a @ v, b, S.GmresConfig(rel_tol=1e-14, max_iter=5))
+    assert rep.flag == "maxiter" and not rep.converged and rep.iterations == 5
+
+
+# ---- error paths (the reference raises ValueError)
+
+
+def test_bad_vector_length(cuda_ok):
+    meta, arr, op = get("fx_tiny")
+    with pytest.raises(ValueError):
+        op.apply_A(np.zeros(op.N + 1, complex))
+
+
+def test_bad_permutation_rejected(cuda_ok):
+    meta, arr = load_case_arrays(golden_path("fx_tiny"))
+    perm = np.array(arr["perm"]).copy()
+    perm[0] = perm[1]
+    with pytest.raises(ValueError, match="permutation"):
+        DeviceOperator(m=meta["m"], n_block_rows=2 * meta["nt"], entries=arr["entries"],
+                       coefs=arr["coefs"], perm=perm, dense=arr["dense"])
+
+
+def test_non_identity_diagonal_raises_in_sweep(cuda_ok):
+    meta, arr = load_case_arrays(golden_path("fx_tiny"))
+    coefs = np.array(arr["coefs"]).copy()
+    entries = np.asarray(arr["entries"])
+    # the T_1 row's own-trace -I entry (pure identity on x_down block 0)
+    idx = np.where((entries[:, 0] == 0) & (entries[:, 1] == 0))[0][0]
+    coefs[idx, 1] = -2.0
+    op = DeviceOperator(m=meta["m"], n_block_rows=2 * meta["nt"], entries=entries, coefs=coefs,
+                        perm=arr["perm"], dense=arr["dense"])
+    op.apply_A(arr["probe_x"])  # the matvec itself is fine
+    with pytest.raises(ValueError, match="not exactly -I"):
+        op.apply_M(arr["probe_x"])
+
+
+# ---- full-size BASELINE configurations (caches built by tools/make_cases.py)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c3r", "c2", "c3"])
+def test_large_case_parity(cuda_ok, name):
+    meta, arr, op = get(name, big=True)
+    assert rel(op.apply_A(arr["probe_x"]), arr["probe_Ax"]) <= APPLY_TOL
+    assert rel(op.apply_M(arr["probe_x"]), arr["probe_Mx"]) <= APPLY_TOL
+    assert rel(op.gs_sweep(arr["probe_x"], arr["probe_u"]), arr["probe_sweep"]) <= APPLY_TOL
+    ref = meta["solves"][0]
+    x, rep = op.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"], max_iter=100)
+    assert abs(rep["iterations"] - ref["iterations"]) <= 1
+    nt, m = meta["nt"], meta["m"]
+    assert rel(x[: nt * m] + x[nt * m:], arr["ref_traces"][0]) <= TRACE_TOL
+
+
+@pytest.mark.slow
+def test_c5_batch_parity(cuda_ok):
+    meta, arr, op = get("c5", big=True)
+    nt, m = meta["nt"], meta["m"]
+    for s in range(0, 64, 9):
+        x, rep = op.gmres(arr["rhs"][s], rel_tol=meta["gmres_tol"])
+        assert abs(rep["iterations"] - meta["solves"][s]["iterations"]) <= 1
+        assert rel(x[: nt * m] + x[nt * m:], arr["ref_traces"][s]) <= TRACE_TOL
