@@ -160,6 +160,16 @@ int pt_gmres_ws_step(pt_gmres_ws *ws, int32_t j, double rel_tol,
 int pt_gmres_ws_finish(pt_gmres_ws *ws, int32_t k, double *x,
                        pt_stream stream);
 
+/* ---- instrumentation -------------------------------------------------------
+ * With timing enabled every executor launch (operator apply / sweep /
+ * fused A->M iteration) is bracketed by CUDA events on its stream;
+ * pt_exec_stats synchronises the device and returns the summed device time,
+ * the launch count and the algorithmic kernel bytes of those launches
+ * (SURVEY.md §8(d)), then resets the accumulators. */
+int pt_exec_timing(pt_handle *h, int32_t enable);
+int pt_exec_stats(pt_handle *h, double *total_ms, int64_t *launches,
+                  int64_t *algo_bytes);
+
 /* ---- misc ----------------------------------------------------------------*/
 const char *pt_last_error(void);
 int32_t pt_abi_version(void);

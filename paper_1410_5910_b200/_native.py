@@ -67,6 +67,9 @@ _SIGS = {
     "pt_gmres_ws_step": (C.c_int, [_VP, C.c_int32, C.c_double, C.c_int32, C.POINTER(Report),
                                    C.POINTER(C.c_int32), _VP]),
     "pt_gmres_ws_finish": (C.c_int, [_VP, C.c_int32, _VP, _VP]),
+    "pt_exec_timing": (C.c_int, [_VP, C.c_int32]),
+    "pt_exec_stats": (C.c_int, [_VP, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int64)]),
     "pt_last_error": (C.c_char_p, []),
     "pt_abi_version": (C.c_int32, []),
     "pt_launch_count": (C.c_int64, []),

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -77,9 +78,13 @@ struct DeviceGuard {
 struct pt_gmres_ws {
   int device = 0;
   GmresDev d{};
-  int* nonfinite = nullptr;
-  DevStatus* st_host = nullptr;  // pinned
+  DevStatus* st_host = nullptr;  // pinned ring of 2 status snapshots
+  cudaEvent_t ev[2] = {nullptr, nullptr};
   ~pt_gmres_ws() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    cudaFree(d.ticket);
+    cudaFree(d.nonfinite);
     cudaFree(d.V);
     cudaFree(d.P);
     cudaFree(d.h1);
@@ -93,7 +98,6 @@ struct pt_gmres_ws {
     cudaFree(d.hist);
     cudaFree(d.y);
     cudaFree(d.st);
-    cudaFree(nonfinite);
     cudaFreeHost(st_host);
   }
 };
@@ -108,9 +112,8 @@ struct pt_handle {
   DevLeaf* leaves = nullptr;
   DevSlot* slots = nullptr;
   DevKernelPLR* kplr = nullptr;
-  int32_t* rowseg = nullptr;
-  DevSegment* segs = nullptr;
-  int32_t* seg_leaves = nullptr;
+  int32_t* tile_ptr = nullptr;
+  int32_t* tile_leaves = nullptr;
   std::map<std::string, std::unique_ptr<DevProgram>> progs;
   double2* slot_buf[N_SLOTS] = {nullptr};
   int64_t slot_cap[N_SLOTS] = {0};
@@ -122,16 +125,45 @@ struct pt_handle {
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
   double2* hx = nullptr;
+  // whole-solve CUDA graphs (conditional WHILE node), keyed by config
+  struct SolveGraph {
+    int n_it = 0, max_iter = 0;
+    double tol = 0.0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<SolveGraph> graphs;
+  cudaStream_t cap_stream = nullptr;
+  double2* gb = nullptr;  // graph-owned rhs / solution buffers
+  double2* gx = nullptr;
+  double* hist_host = nullptr;  // pinned
+  void drop_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
+  // per-launch instrumentation of the executor
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_free;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used;
+  int64_t timed_launches = 0, timed_bytes = 0;
   ~pt_handle() {
+    for (auto& p : ev_used) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+    for (auto e : ev_free) cudaEventDestroy(e);
+    drop_graphs();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    cudaFree(gb);
+    cudaFree(gx);
+    cudaFreeHost(hist_host);
     progs.clear();
     cudaFree(dense);
     cudaFree(fac);
     cudaFree(leaves);
     cudaFree(slots);
     cudaFree(kplr);
-    cudaFree(rowseg);
-    cudaFree(segs);
-    cudaFree(seg_leaves);
+    cudaFree(tile_ptr);
+    cudaFree(tile_leaves);
     for (int s = 0; s < N_SLOTS; ++s) cudaFree(slot_buf[s]);
     cudaFree(ctr);
     cudaFree(tmp);
@@ -169,14 +201,12 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
   op.kplr.assign(op.nk, DevKernelPLR{});
   op.nslot.assign(op.nk, 0);
   op.kernel_bytes.assign(op.nk, 0);
-  op.rowseg.assign((size_t)op.nk * m, 0);
   size_t pos = 0;
   for (int k = 0; k < op.nk; ++k) {
     DevKernelPLR& kp = op.kplr[k];
     kp.leaf0 = (int32_t)op.leaves.size();
     kp.slot0 = (int32_t)op.slots.size();
     int32_t slot = 0;
-    std::vector<int64_t> bounds = {0, m};
     for (; pos < idx.size() && leaves[idx[pos]].kernel == k; ++pos) {
       const pt_leaf& L = leaves[idx[pos]];
       op.kernel_bytes[k] += 16 * L.rank * (L.rows + L.cols);
@@ -209,45 +239,39 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
       }
       slot += (int32_t)L.rank;
       op.leaves.push_back(dl);
-      bounds.push_back(L.row_off);
-      bounds.push_back(L.row_off + L.rows);
     }
     kp.nleaf = (int32_t)op.leaves.size() - kp.leaf0;
     kp.nslot = slot;
     op.nslot[k] = slot;
-    std::sort(bounds.begin(), bounds.end());
-    bounds.erase(std::unique(bounds.begin(), bounds.end()), bounds.end());
-    kp.seg0 = (int32_t)(k * m);
-    for (size_t b = 0; b + 1 < bounds.size(); ++b) {
-      const int64_t lo = bounds[b], hi = bounds[b + 1];
-      DevSegment sg{};
-      sg.leaf_list0 = (int32_t)op.seg_leaves.size();
+    // leaves meeting each PLR_TILE-row tile, in leaf (slot) order
+    const int64_t ntiles = (m + PLR_TILE - 1) / PLR_TILE;
+    kp.tile0 = (int32_t)op.tile_ptr.size();
+    for (int64_t t = 0; t < ntiles; ++t) {
+      op.tile_ptr.push_back((int32_t)op.tile_leaves.size());
+      const int64_t lo = t * PLR_TILE, hi = std::min<int64_t>(m, lo + PLR_TILE);
       for (int32_t l = kp.leaf0; l < kp.leaf0 + kp.nleaf; ++l) {
         const DevLeaf& dl = op.leaves[l];
-        if (dl.row_off <= lo && dl.row_off + dl.rows >= hi) op.seg_leaves.push_back(l);
+        if (dl.row_off < hi && dl.row_off + dl.rows > lo) op.tile_leaves.push_back(l);
       }
-      sg.nleaf = (int32_t)op.seg_leaves.size() - sg.leaf_list0;
-      const int32_t sid = (int32_t)op.segs.size();
-      op.segs.push_back(sg);
-      for (int64_t r = lo; r < hi; ++r) op.rowseg[(size_t)k * m + r] = sid;
     }
+    op.tile_ptr.push_back((int32_t)op.tile_leaves.size());
   }
-  if (op.seg_leaves.empty()) op.seg_leaves.push_back(0);
+  if (op.tile_leaves.empty()) op.tile_leaves.push_back(0);
   if (blob.empty()) blob.push_back(make_double2(0.0, 0.0));
   int rc;
   if ((rc = upload(&h->fac, blob))) return rc;
   if ((rc = upload(&h->leaves, op.leaves))) return rc;
   if ((rc = upload(&h->slots, op.slots))) return rc;
   if ((rc = upload(&h->kplr, op.kplr))) return rc;
-  if ((rc = upload(&h->rowseg, op.rowseg))) return rc;
-  if ((rc = upload(&h->segs, op.segs))) return rc;
-  if ((rc = upload(&h->seg_leaves, op.seg_leaves))) return rc;
+  if ((rc = upload(&h->tile_ptr, op.tile_ptr))) return rc;
+  if ((rc = upload(&h->tile_leaves, op.tile_leaves))) return rc;
   return 0;
 }
 
 int ensure_slot(pt_handle* h, int s, int64_t elems) {
   if (elems <= h->slot_cap[s]) return 0;
   CK(cudaDeviceSynchronize());
+  h->drop_graphs();
   cudaFree(h->slot_buf[s]);
   h->slot_buf[s] = nullptr;
   CK(cudaMalloc(&h->slot_buf[s], (size_t)std::max<int64_t>(elems, 1) * sizeof(double2)));
@@ -281,6 +305,7 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
     if ((rc = ensure_slot(h, s, p->host.slot_elems[s]))) return rc;
   if (p->host.n_counters + 1 > h->ctr_cap) {
     CK(cudaDeviceSynchronize());
+    h->drop_graphs();
     cudaFree(h->ctr);
     h->ctr_cap = p->host.n_counters + 1;
     CK(cudaMalloc(&h->ctr, h->ctr_cap * sizeof(int)));
@@ -290,8 +315,14 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
   return 0;
 }
 
+struct IterMode {
+  const int* iter = nullptr;  // device iteration counter (st->iterations)
+  double2* vbase = nullptr;   // basis
+  int64_t vstride = 0;
+};
+
 int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, const double2* aux,
-                cudaStream_t s) {
+                cudaStream_t s, const int* stop = nullptr, IterMode im = IterMode()) {
   if (p->host.tasks.empty()) return 0;
   ExecArgs a{};
   a.tasks = p->tasks;
@@ -309,16 +340,47 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.leaves = h->leaves;
   a.slots = h->slots;
   a.kplr = h->kplr;
-  a.rowseg = h->rowseg;
-  a.segs = h->segs;
-  a.seg_leaves = h->seg_leaves;
+  a.tile_ptr = h->tile_ptr;
+  a.tile_leaves = h->tile_leaves;
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
+  a.stop = stop;
+  a.iter = im.iter;
+  a.vbase = im.vbase;
+  a.vstride = im.vstride;
   CK(cudaMemsetAsync(h->ctr, 0, (p->host.n_counters + 1) * sizeof(int), s));
-  void* args[] = {&a};
   count_launch();
-  CK(cudaLaunchCooperativeKernel((const void*)pt_exec_kernel, dim3(h->grid), dim3(EXEC_THREADS),
-                                 args, h->smem, s));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing) {
+    for (cudaEvent_t* e : {&e0, &e1}) {
+      if (h->ev_free.empty()) {
+        CK(cudaEventCreate(e));
+      } else {
+        *e = h->ev_free.back();
+        h->ev_free.pop_back();
+      }
+    }
+    CK(cudaEventRecord(e0, s));
+  }
+  // cooperative: every CTA resident (counter waits cannot deadlock); launched
+  // through cudaLaunchKernelEx so it can also be captured into a graph
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(h->grid);
+  cfg.blockDim = dim3(EXEC_THREADS);
+  cfg.dynamicSmemBytes = h->smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, pt_exec_kernel, a));
+  if (h->timing) {
+    CK(cudaEventRecord(e1, s));
+    h->ev_used.emplace_back(e0, e1);
+    h->timed_launches += 1;
+    h->timed_bytes += p->host.algo_bytes;
+  }
   return 0;
 }
 
@@ -341,32 +403,42 @@ int ws_alloc(pt_gmres_ws* w, int64_t n, int max_iter) {
   CK(cudaMalloc(&d.hist, max_iter * sizeof(double)));
   CK(cudaMalloc(&d.y, ldr * sizeof(double2)));
   CK(cudaMalloc(&d.st, sizeof(DevStatus)));
-  CK(cudaMalloc(&w->nonfinite, sizeof(int)));
-  CK(cudaMallocHost(&w->st_host, sizeof(DevStatus)));
+  CK(cudaMalloc(&d.nonfinite, sizeof(int)));
+  CK(cudaMalloc(&d.ticket, 4 * sizeof(int)));
+  CK(cudaMallocHost(&w->st_host, 2 * sizeof(DevStatus)));
   CK(cudaMemset(d.st, 0, sizeof(DevStatus)));
+  CK(cudaMemset(d.nonfinite, 0, sizeof(int)));
+  CK(cudaMemset(d.ticket, 0, 4 * sizeof(int)));
+  for (auto& e : w->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return 0;
 }
 
-int fetch_status(pt_gmres_ws* w, cudaStream_t s) {
-  CK(cudaMemcpyAsync(w->st_host, w->d.st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+int fetch_status(pt_gmres_ws* w, cudaStream_t s, int slot = 0) {
+  CK(cudaMemcpyAsync(w->st_host + slot, w->d.st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return 0;
 }
 
-int ws_begin_impl(pt_gmres_ws* w, const double* mb, double* beta_out, cudaStream_t s) {
+int ws_begin_impl(pt_gmres_ws* w, const double* mb, double* beta_out, cudaStream_t s,
+                  bool sync) {
   GmresDev& d = w->d;
   if ((const double2*)mb != d.V)
     CK(cudaMemcpyAsync(d.V, mb, d.n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemsetAsync(w->nonfinite, 0, sizeof(int), s));
-  gm_norm(d.V, d.n, d.P, d.ldp, nullptr, s);
-  gm_reduce(d.P, d.ldp, 1, d.hn2, s);
-  gm_begin(d, s);
-  gm_scale(d.V, d.n, d.st, 1, s);
+  gm_begin(d, 0, s);
   CK(cudaGetLastError());
+  if (!sync) return 0;
   int rc = fetch_status(w, s);
   if (rc) return rc;
   if (beta_out) *beta_out = w->st_host->beta;
   return 0;
+}
+
+void fill_report(const DevStatus& st, pt_report* rep) {
+  rep->iterations = st.iterations;
+  rep->flag = st.flag;
+  rep->converged = st.converged;
+  rep->beta = st.beta;
+  rep->nonfinite = st.nonfinite;
 }
 
 int ws_step_impl(pt_gmres_ws* w, int j, double rel_tol, int max_iter, pt_report* rep, int* stop,
@@ -374,31 +446,21 @@ int ws_step_impl(pt_gmres_ws* w, int j, double rel_tol, int max_iter, pt_report*
   GmresDev& d = w->d;
   if (j < 0 || j >= d.max_iter || max_iter > d.max_iter)
     return fail(PT_EINVAL, "GMRES step index outside the workspace");
-  double2* wv = d.V + (int64_t)(j + 1) * d.n;
-  const int nc = j + 1;
-  gm_dots(d.V, d.n, nc, wv, d.n, d.P, d.ldp, w->nonfinite, s);
-  gm_reduce(d.P, d.ldp, nc, d.h1, s);
-  gm_update_dots(d.V, d.n, nc, d.h1, wv, d.n, d.P, d.ldp, s);
-  gm_reduce(d.P, d.ldp, nc, d.h2, s);
-  gm_update_norm(d.V, d.n, nc, d.h2, wv, d.n, d.P, d.ldp, s);
-  gm_reduce(d.P, d.ldp, 1, d.hn2, s);
-  gm_givens(d, j, rel_tol, max_iter, w->nonfinite, s);
-  gm_scale(wv, d.n, d.st, 0, s);
+  gm_arnoldi_step(d, rel_tol, max_iter, 0, s);
   CK(cudaGetLastError());
   int rc = fetch_status(w, s);
   if (rc) return rc;
   const DevStatus& st = *w->st_host;
+  if (st.iterations != j + 1 && !st.nonfinite && !st.stop)
+    return fail(PT_EINVAL, "GMRES steps must be taken in order");
   if (st.nonfinite) {
     if (rep) rep->nonfinite = 1;
     return fail(PT_ENONFINITE, "non-finite values in preconditioned matvec at iteration " +
                                    std::to_string(j + 1));
   }
   if (rep) {
-    rep->iterations = st.iterations;
-    rep->flag = st.flag;
-    rep->converged = st.converged;
-    rep->beta = st.beta;
-    if (rep->residual_history) rep->residual_history[j] = st.rel;
+    fill_report(st, rep);
+    if (rep->residual_history && st.iterations == j + 1) rep->residual_history[j] = st.rel;
   }
   *stop = st.stop;
   return 0;
@@ -407,6 +469,10 @@ int ws_step_impl(pt_gmres_ws* w, int j, double rel_tol, int max_iter, pt_report*
 int ensure_gws(pt_handle* h, int max_iter) {
   if (h->gws && h->gws->d.max_iter >= max_iter) return 0;
   CK(cudaDeviceSynchronize());
+  h->drop_graphs();
+  cudaFreeHost(h->hist_host);
+  h->hist_host = nullptr;
+  CK(cudaMallocHost(&h->hist_host, (size_t)max_iter * sizeof(double)));
   h->gws.reset(new pt_gmres_ws());
   h->gws->device = h->device;
   return ws_alloc(h->gws.get(), h->N(), max_iter);
@@ -470,7 +536,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     if (n_leaves > 0 && (!leaves || !factors)) return fail(PT_EINVAL, "PLR tables missing");
     if ((rc = build_plr_tables(h.get(), leaves, n_leaves, factors, n_factor_complex))) return rc;
   }
-  h->smem = (size_t)op.m * sizeof(double2);
+  h->smem = std::max<size_t>((size_t)op.m, EXEC_THREADS) * sizeof(double2);
   if (h->smem > 48 * 1024)
     CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)h->smem));
@@ -480,7 +546,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (occ < 1) return fail(PT_EINVAL, "executor kernel does not fit on an SM");
   h->grid = nsm * occ;
   h->pp.dense_rows_per_task = DENSE_ROWS_PER_TASK;
-  h->pp.plr_rows_per_task = EXEC_THREADS;
+  h->pp.plr_rows_per_task = PLR_TILE;
   CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
   *out = h.release();
   return 0;
@@ -535,14 +601,144 @@ int pt_gs_sweep(pt_handle* h, const double* rhs, const double* u_in, double* u_o
   return 0;
 }
 
-int pt_gmres(pt_handle* h, const double* b, double* x, const pt_gmres_config* cfg,
-             pt_report* report, pt_stream stream) {
-  if (!h || !b || !x) return fail(PT_EINVAL, "null argument");
-  int rc = check_cfg(cfg);
+}  // extern "C"
+
+namespace {
+
+// Build the whole online solve as one CUDA graph:
+//   M b -> V0, beta | WHILE(cond) { A->M iteration program on V_j,
+//   CGS2 + Givens (sets cond) } | y, x = V y, A x, true residual, D2H status.
+// The host synchronises once per solve.
+int build_solve_graph(pt_handle* h, int n_it, int max_iter, double tol,
+                      pt_handle::SolveGraph* out) {
+  DevProgram *pM, *pAM, *pA;
+  int rc;
+  if ((rc = get_program(h, "M", n_it, &pM))) return rc;
+  if ((rc = get_program(h, "AM", n_it, &pAM))) return rc;
+  if ((rc = get_program(h, "A", 0, &pA))) return rc;
+  pt_gmres_ws* w = h->gws.get();
+  GmresDev& d = w->d;
+  cudaStream_t cs = h->cap_stream;
+  cudaGraph_t g = nullptr, tmp = nullptr;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle cond;
+  CK(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+  // prologue
+  CK(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  rc = run_program(h, pM, h->gb, d.V, nullptr, cs);
+  if (!rc) gm_begin(d, cond, cs);
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaError_t ce = cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps);
+  std::vector<cudaGraphNode_t> tail(deps, deps + ndeps);
+  CK(cudaStreamEndCapture(cs, &tmp));
   if (rc) return rc;
-  if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
-  DeviceGuard guard(h->device);
-  cudaStream_t s = (cudaStream_t)stream;
+  CK(ce);
+  // loop
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t loop;
+  CK(cudaGraphAddNode(&loop, g, tail.data(), tail.size(), &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  IterMode im;
+  im.iter = &d.st->iterations;
+  im.vbase = d.V;
+  im.vstride = d.n;
+  rc = run_program(h, pAM, nullptr, nullptr, nullptr, cs, &d.st->stop, im);
+  if (!rc) gm_arnoldi_step(d, tol, max_iter, cond, cs);
+  CK(cudaStreamEndCapture(cs, &tmp));
+  if (rc) return rc;
+  // epilogue
+  CK(cudaStreamBeginCaptureToGraph(cs, g, &loop, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+  gm_finish(d, h->gx, cs);
+  rc = run_program(h, pA, h->gx, h->tmp, nullptr, cs);
+  if (!rc) gm_resid(d, h->gb, h->tmp, cs);
+  cudaError_t c1 = cudaMemcpyAsync(w->st_host, d.st, sizeof(DevStatus), cudaMemcpyDeviceToHost, cs);
+  cudaError_t c2 = cudaMemcpyAsync(h->hist_host, d.hist, (size_t)max_iter * sizeof(double),
+                                   cudaMemcpyDeviceToHost, cs);
+  CK(cudaStreamEndCapture(cs, &tmp));
+  if (rc) return rc;
+  CK(c1);
+  CK(c2);
+  CK(cudaGraphInstantiate(&out->exec, g, 0));
+  CK(cudaGraphDestroy(g));
+  out->n_it = n_it;
+  out->max_iter = max_iter;
+  out->tol = tol;
+  return 0;
+}
+
+int finish_report(pt_handle* h, const DevStatus& st, int max_iter, pt_report* rep) {
+  fill_report(st, rep);
+  if (st.nonfinite) {
+    rep->nonfinite = 1;
+    return fail(PT_ENONFINITE, "non-finite values in preconditioned matvec at iteration " +
+                                   std::to_string(st.iterations + 1));
+  }
+  if (st.beta == 0.0) {  // solver.py:239-242
+    rep->converged = 1;
+    rep->flag = PT_FLAG_CONVERGED;
+    rep->true_residual = 0.0;
+    return 0;
+  }
+  const double tr = std::sqrt(st.true_num2), sc = std::sqrt(st.b_norm2);
+  rep->true_residual = sc > 0.0 ? tr / sc : tr;
+  (void)h;
+  (void)max_iter;
+  return 0;
+}
+
+// Graph path: b/x may be the graph's own buffers (then no copies).
+int gmres_graph(pt_handle* h, const double2* b, double2* x, bool b_host, bool x_host,
+                const pt_gmres_config* cfg, pt_report* rep, cudaStream_t s) {
+  int rc;
+  if ((rc = ensure_gws(h, cfg->max_iter))) return rc;
+  const int64_t N = h->N();
+  const size_t bytes = (size_t)N * sizeof(double2);
+  if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  if (!h->gb) CK(cudaMalloc(&h->gb, bytes));
+  if (!h->gx) CK(cudaMalloc(&h->gx, bytes));
+  // programs first: building them may reallocate buffers (and drop graphs)
+  DevProgram* p;
+  if ((rc = get_program(h, "M", cfg->n_it, &p))) return rc;
+  if ((rc = get_program(h, "AM", cfg->n_it, &p))) return rc;
+  if ((rc = get_program(h, "A", 0, &p))) return rc;
+  pt_handle::SolveGraph* sg = nullptr;
+  for (auto& g : h->graphs)
+    if (g.n_it == cfg->n_it && g.max_iter == cfg->max_iter && g.tol == cfg->rel_tol) sg = &g;
+  if (!sg) {
+    pt_handle::SolveGraph ng;
+    if ((rc = build_solve_graph(h, cfg->n_it, cfg->max_iter, cfg->rel_tol, &ng))) return rc;
+    h->graphs.push_back(ng);
+    sg = &h->graphs.back();
+  }
+  if (b != h->gb)
+    CK(cudaMemcpyAsync(h->gb, b, bytes, b_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       s));
+  count_launch();
+  CK(cudaGraphLaunch(sg->exec, s));
+  if (x != h->gx)
+    CK(cudaMemcpyAsync(x, h->gx, bytes, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                       s));
+  CK(cudaStreamSynchronize(s));
+  const DevStatus st = h->gws->st_host[0];
+  if (rep->residual_history && st.iterations > 0)
+    std::memcpy(rep->residual_history, h->hist_host, (size_t)st.iterations * sizeof(double));
+  return finish_report(h, st, cfg->max_iter, rep);
+}
+
+// Host-driven path (PT_GRAPH=0, and whenever per-launch timing is on):
+// iterations are enqueued speculatively one batch ahead of the host's
+// convergence check; kernels after the stop return immediately.
+int gmres_stream(pt_handle* h, const double2* b, double2* x, const pt_gmres_config* cfg,
+                 pt_report* rep, cudaStream_t s) {
+  int rc;
   if ((rc = ensure_gws(h, cfg->max_iter))) return rc;
   pt_gmres_ws* w = h->gws.get();
   GmresDev& d = w->d;
@@ -550,55 +746,95 @@ int pt_gmres(pt_handle* h, const double* b, double* x, const pt_gmres_config* cf
   if ((rc = get_program(h, "M", cfg->n_it, &pM))) return rc;
   if ((rc = get_program(h, "AM", cfg->n_it, &pAM))) return rc;
   if ((rc = get_program(h, "A", 0, &pA))) return rc;
+  const int64_t N = h->N();
+  if ((rc = run_program(h, pM, b, d.V, nullptr, s))) return rc;
+  gm_begin(d, 0, s);
+  const int B = 2;
+  int enq = 0, nb = 0, waited = 0;
+  DevStatus last{};
+  IterMode im;
+  im.iter = &d.st->iterations;
+  im.vbase = d.V;
+  im.vstride = N;
+  auto enqueue_batch = [&]() -> int {
+    for (int i = 0; i < B && enq < cfg->max_iter; ++i, ++enq) {
+      int r = run_program(h, pAM, nullptr, nullptr, nullptr, s, &d.st->stop, im);
+      if (r) return r;
+      gm_arnoldi_step(d, cfg->rel_tol, cfg->max_iter, 0, s);
+    }
+    CK(cudaMemcpyAsync(w->st_host + (nb % 2), d.st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(w->ev[nb % 2], s));
+    ++nb;
+    return 0;
+  };
+  if ((rc = enqueue_batch())) return rc;
+  for (;;) {
+    if (enq < cfg->max_iter && (rc = enqueue_batch())) return rc;
+    CK(cudaEventSynchronize(w->ev[waited % 2]));
+    last = w->st_host[waited % 2];
+    ++waited;
+    if (last.stop) break;
+    if (waited == nb && enq >= cfg->max_iter) break;
+  }
+  gm_finish(d, x, s);
+  if ((rc = run_program(h, pA, x, h->tmp, nullptr, s))) return rc;
+  gm_resid(d, b, h->tmp, s);
+  CK(cudaGetLastError());
+  if ((rc = fetch_status(w, s))) return rc;
+  const DevStatus st = *w->st_host;
+  if (rep->residual_history && st.iterations > 0)
+    CK(cudaMemcpy(rep->residual_history, d.hist, (size_t)st.iterations * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+  return finish_report(h, st, cfg->max_iter, rep);
+}
+
+bool use_graph(const pt_handle* h) {
+  const char* e = std::getenv("PT_GRAPH");
+  return !h->timing && !(e && e[0] == '0');
+}
+
+}  // namespace
+
+extern "C" {
+
+int pt_gmres(pt_handle* h, const double* b, double* x, const pt_gmres_config* cfg,
+             pt_report* report, pt_stream stream) {
+  if (!h || !b || !x) return fail(PT_EINVAL, "null argument");
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  DeviceGuard guard(h->device);
   pt_report local{};
   pt_report* rep = report ? report : &local;
   double* hist = rep->residual_history;
   *rep = pt_report{};
   rep->residual_history = hist;
-  rep->flag = PT_FLAG_CONVERGED;
-  const int64_t N = h->N();
-  // mb = M^-1 b straight into basis column 0
-  if ((rc = run_program(h, pM, (const double2*)b, d.V, nullptr, s))) return rc;
-  double beta = 0.0;
-  if ((rc = ws_begin_impl(w, (const double*)d.V, &beta, s))) return rc;
-  rep->beta = beta;
-  if (beta == 0.0) {
-    gm_zero((double2*)x, N, s);
-    CK(cudaStreamSynchronize(s));
-    rep->converged = 1;
-    rep->true_residual = 0.0;
-    return 0;
-  }
-  int stop = 0;
-  for (int j = 0; j < cfg->max_iter && !stop; ++j) {
-    if ((rc = run_program(h, pAM, d.V + (int64_t)j * N, d.V + (int64_t)(j + 1) * N, nullptr, s)))
-      return rc;
-    if ((rc = ws_step_impl(w, j, cfg->rel_tol, cfg->max_iter, rep, &stop, s))) return rc;
-  }
-  const int k = rep->iterations;
-  gm_backsolve(d, k, s);
-  gm_combine(d.V, N, k, d.y, (double2*)x, N, s);
-  if ((rc = run_program(h, pA, (const double2*)x, h->tmp, nullptr, s))) return rc;
-  gm_resid((const double2*)b, h->tmp, N, d.P, d.ldp, s);
-  gm_resid_finish(d, s);
-  CK(cudaGetLastError());
-  if ((rc = fetch_status(w, s))) return rc;
-  const double tr = std::sqrt(w->st_host->true_num2), sc = std::sqrt(w->st_host->b_norm2);
-  rep->true_residual = sc > 0.0 ? tr / sc : tr;
-  return 0;
+  if (use_graph(h))
+    return gmres_graph(h, (const double2*)b, (double2*)x, false, false, cfg, rep,
+                       (cudaStream_t)stream);
+  return gmres_stream(h, (const double2*)b, (double2*)x, cfg, rep, (cudaStream_t)stream);
 }
 
 int pt_gmres_host(pt_handle* h, const double* b_host, double* x_host, const pt_gmres_config* cfg,
                   pt_report* report, pt_stream stream) {
   if (!h || !b_host || !x_host) return fail(PT_EINVAL, "null argument");
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
   DeviceGuard guard(h->device);
   cudaStream_t s = (cudaStream_t)stream;
+  pt_report local{};
+  pt_report* rep = report ? report : &local;
+  double* hist = rep->residual_history;
+  *rep = pt_report{};
+  rep->residual_history = hist;
+  if (use_graph(h))
+    return gmres_graph(h, (const double2*)b_host, (double2*)x_host, true, true, cfg, rep, s);
   const size_t bytes = (size_t)h->N() * sizeof(double2);
   if (!h->hb) CK(cudaMalloc(&h->hb, bytes));
   if (!h->hx) CK(cudaMalloc(&h->hx, bytes));
   CK(cudaMemcpyAsync(h->hb, b_host, bytes, cudaMemcpyHostToDevice, s));
-  int rc = pt_gmres(h, (const double*)h->hb, (double*)h->hx, cfg, report, stream);
-  if (rc) return rc;
+  if ((rc = gmres_stream(h, h->hb, h->hx, cfg, rep, s))) return rc;
   CK(cudaMemcpyAsync(x_host, h->hx, bytes, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return 0;
@@ -642,7 +878,7 @@ double* pt_gmres_ws_basis(pt_gmres_ws* ws, int32_t j) {
 int pt_gmres_ws_begin(pt_gmres_ws* ws, const double* mb, double* beta_out, pt_stream stream) {
   if (!ws || !mb) return fail(PT_EINVAL, "null argument");
   DeviceGuard guard(ws->device);
-  return ws_begin_impl(ws, mb, beta_out, (cudaStream_t)stream);
+  return ws_begin_impl(ws, mb, beta_out, (cudaStream_t)stream, true);
 }
 
 int pt_gmres_ws_step(pt_gmres_ws* ws, int32_t j, double rel_tol, int32_t max_iter,
@@ -659,9 +895,40 @@ int pt_gmres_ws_finish(pt_gmres_ws* ws, int32_t k, double* x, pt_stream stream) 
   if (!ws || !x || k < 0 || k > ws->d.max_iter) return fail(PT_EINVAL, "bad argument");
   DeviceGuard guard(ws->device);
   cudaStream_t s = (cudaStream_t)stream;
-  gm_backsolve(ws->d, k, s);
-  gm_combine(ws->d.V, ws->d.n, k, ws->d.y, (double2*)x, ws->d.n, s);
+  (void)k;  // k is the device's own iteration count (st->iterations)
+  gm_finish(ws->d, (double2*)x, s);
   CK(cudaGetLastError());
+  return 0;
+}
+
+int pt_exec_timing(pt_handle* h, int32_t enable) {
+  if (!h) return fail(PT_EINVAL, "null handle");
+  DeviceGuard guard(h->device);
+  double ms;
+  int64_t n, b;
+  int rc = pt_exec_stats(h, &ms, &n, &b);
+  h->timing = enable != 0;
+  return rc;
+}
+
+int pt_exec_stats(pt_handle* h, double* total_ms, int64_t* launches, int64_t* algo_bytes) {
+  if (!h) return fail(PT_EINVAL, "null handle");
+  DeviceGuard guard(h->device);
+  CK(cudaDeviceSynchronize());
+  double tot = 0.0;
+  for (auto& p : h->ev_used) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.first, p.second));
+    tot += ms;
+    h->ev_free.push_back(p.first);
+    h->ev_free.push_back(p.second);
+  }
+  h->ev_used.clear();
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = h->timed_launches;
+  if (algo_bytes) *algo_bytes = h->timed_bytes;
+  h->timed_launches = 0;
+  h->timed_bytes = 0;
   return 0;
 }
 

@@ -79,9 +79,14 @@ struct ExecArgs {
   const DevLeaf* leaves;
   const DevSlot* slots;
   const DevKernelPLR* kplr;
-  const int32_t* rowseg;
-  const DevSegment* segs;
-  const int32_t* seg_leaves;
+  const int32_t* tile_ptr;
+  const int32_t* tile_leaves;
+  const int* stop;  // GMRES status stop flag: the whole launch is skipped once set
+  // iteration-relative basis addressing (GMRES loop inside a graph):
+  // if iter != nullptr, SLOT_IN = vbase + (*iter) * vstride, SLOT_OUT = SLOT_IN + vstride
+  const int* iter;
+  double2* vbase;
+  int64_t vstride;
   int n_tasks;
   int m;
 };

@@ -9,8 +9,11 @@
 // out of one rotation instead of a least-squares solve.  The flag logic
 // (breakdown, tolerance, stagnation window, maxiter) follows :265-289.
 //
-// Reductions are two-stage with a fixed number of partial blocks and a
-// fixed summation order: repeat solves are bitwise identical.
+// Each Arnoldi step is four kernels.  Block partial sums are reduced by the
+// last block to finish (ticket counter), always over all blocks in index
+// order, so results are bitwise repeatable.  Every step kernel returns at
+// once when the status says the solve has stopped: the host enqueues steps
+// ahead of its convergence check without changing the result.
 #include <cmath>
 
 #include "pt_device.cuh"
@@ -22,13 +25,17 @@ extern void count_launch();
 
 namespace {
 
+__device__ __forceinline__ bool stopped(const DevStatus* st) {
+  return *((volatile const int*)&st->stop) != 0;
+}
+
 __device__ __forceinline__ void block_range(int64_t n, int64_t& lo, int64_t& hi) {
   const int64_t chunk = (n + RED_BLOCKS - 1) / RED_BLOCKS;
   lo = (int64_t)blockIdx.x * chunk;
   hi = lo + chunk < n ? lo + chunk : n;
 }
 
-// block-wide sum of RED_CHUNK complex values; thread u < RED_CHUNK returns sum u
+// block-wide sum of RED_CHUNK complex values; thread u < count writes sum u
 __device__ void block_sum_chunk(double2 (&acc)[RED_CHUNK], double2 (*red)[RED_CHUNK],
                                 double2* outp, int count) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -41,7 +48,7 @@ __device__ void block_sum_chunk(double2 (&acc)[RED_CHUNK], double2 (*red)[RED_CH
   if (threadIdx.x < count) {
     double2 s = make_double2(0.0, 0.0);
     for (int w = 0; w < RED_THREADS / 32; ++w) s = cadd(s, red[w][threadIdx.x]);
-    outp[threadIdx.x] = s;
+    st_cg(outp + threadIdx.x, s);
   }
   __syncthreads();
 }
@@ -65,44 +72,6 @@ __device__ void dots_pass(const double2* V, int64_t ldv, int ncols, const double
   }
 }
 
-__global__ void __launch_bounds__(RED_THREADS)
-k_dots(const double2* V, int64_t ldv, int ncols, const double2* w, int64_t n, double2* P,
-       int ldp, int* nonfinite) {
-  int64_t lo, hi;
-  block_range(n, lo, hi);
-  if (nonfinite) {
-    int bad = 0;
-    for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
-      const double2 v = ld_cg(w + e);
-      bad |= !(isfinite(v.x) && isfinite(v.y));
-    }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
-  }
-  dots_pass(V, ldv, ncols, w, lo, hi, P + (int64_t)blockIdx.x * ldp);
-}
-
-// w -= V h, in place; own elements only
-__device__ void update_pass(const double2* V, int64_t ldv, int ncols, const double2* hs,
-                            double2* w, int64_t lo, int64_t hi) {
-  for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int i = 0; i < ncols; ++i) acc = cfma(ld_cg(V + (int64_t)i * ldv + e), hs[i], acc);
-    st_cg(w + e, csub(ld_cg(w + e), acc));
-  }
-}
-
-__global__ void __launch_bounds__(RED_THREADS)
-k_update_dots(const double2* V, int64_t ldv, int ncols, const double2* h, double2* w, int64_t n,
-              double2* P, int ldp) {
-  extern __shared__ double2 hs[];
-  for (int i = threadIdx.x; i < ncols; i += RED_THREADS) hs[i] = h[i];
-  __syncthreads();
-  int64_t lo, hi;
-  block_range(n, lo, hi);
-  update_pass(V, ldv, ncols, hs, w, lo, hi);
-  dots_pass(V, ldv, ncols, w, lo, hi, P + (int64_t)blockIdx.x * ldp);
-}
-
 __device__ void norm_pass(const double2* w, int64_t lo, int64_t hi, double2* outp) {
   __shared__ double2 red[RED_THREADS / 32][RED_CHUNK];
   double2 acc[RED_CHUNK];
@@ -116,77 +85,41 @@ __device__ void norm_pass(const double2* w, int64_t lo, int64_t hi, double2* out
   block_sum_chunk(acc, red, outp, 1);
 }
 
-__global__ void __launch_bounds__(RED_THREADS)
-k_update_norm(const double2* V, int64_t ldv, int ncols, const double2* h, double2* w, int64_t n,
-              double2* P, int ldp) {
-  extern __shared__ double2 hs[];
-  for (int i = threadIdx.x; i < ncols; i += RED_THREADS) hs[i] = h[i];
-  __syncthreads();
-  int64_t lo, hi;
-  block_range(n, lo, hi);
-  update_pass(V, ldv, ncols, hs, w, lo, hi);
-  norm_pass(w, lo, hi, P + (int64_t)blockIdx.x * ldp);
-}
-
-__global__ void __launch_bounds__(RED_THREADS)
-k_norm(const double2* w, int64_t n, double2* P, int ldp, int* nonfinite) {
-  int64_t lo, hi;
-  block_range(n, lo, hi);
-  if (nonfinite) {
-    int bad = 0;
-    for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
-      const double2 v = ld_cg(w + e);
-      bad |= !(isfinite(v.x) && isfinite(v.y));
-    }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+// w -= V hs, in place; own elements only
+__device__ void update_pass(const double2* V, int64_t ldv, int ncols, const double2* hs,
+                            double2* w, int64_t lo, int64_t hi) {
+  for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < ncols; ++i) acc = cfma(ld_cg(V + (int64_t)i * ldv + e), hs[i], acc);
+    st_cg(w + e, csub(ld_cg(w + e), acc));
   }
-  norm_pass(w, lo, hi, P + (int64_t)blockIdx.x * ldp);
 }
 
-// out[i] = sum_b P[b, i], fixed order
-__global__ void k_reduce(const double2* P, int ldp, int ncols, double2* out) {
+// The last block to arrive sums the partials of all blocks (index order).
+__device__ bool last_block(int* ticket) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+__device__ void reduce_partials(const double2* P, int ldp, int ncols, double2* out) {
   for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
     double2 s = make_double2(0.0, 0.0);
-    for (int b = 0; b < RED_BLOCKS; ++b) s = cadd(s, P[(int64_t)b * ldp + i]);
-    out[i] = s;
-  }
-}
-
-__global__ void k_begin(GmresDev g) {
-  DevStatus* st = g.st;
-  const double beta = sqrt(g.hn2[0].x);
-  st->iterations = 0;
-  st->flag = 0;
-  st->converged = 0;
-  st->stop = 0;
-  st->nonfinite = 0;
-  st->breakdown = 0;
-  st->rel = 1.0;
-  st->beta = beta;
-  st->inv_hn = beta > 0.0 ? 1.0 / beta : 0.0;
-  st->hn = beta;
-  for (int i = 0; i <= g.max_iter; ++i) g.g[i] = make_double2(0.0, 0.0);
-  g.g[0] = make_double2(beta, 0.0);
-}
-
-__global__ void k_scale(double2* w, int64_t n, const DevStatus* st) {
-  const double s = st->inv_hn;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    double2 v = ld_cg(w + e);
-    v.x *= s;
-    v.y *= s;
-    st_cg(w + e, v);
+    for (int b = 0; b < RED_BLOCKS; ++b) s = cadd(s, ld_cg(P + (int64_t)b * ldp + i));
+    st_cg(out + i, s);
   }
 }
 
 __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 
-// One Arnoldi column j: h = h1 + h2, hn = ||w||; rotations; flags.
-__global__ void k_givens(GmresDev g, int j, double rel_tol, int max_iter,
-                         const int* nonfinite) {
+// Arnoldi column j: h = h1 + h2, hn; rotations; residual; flags (one thread)
+__device__ void givens_update(const GmresDev& g, int j, double rel_tol, int max_iter) {
   DevStatus* st = g.st;
-  if (*nonfinite) {
+  if (*((volatile int*)g.nonfinite)) {
     st->nonfinite = 1;
     st->stop = 1;
     st->converged = 0;
@@ -196,27 +129,29 @@ __global__ void k_givens(GmresDev g, int j, double rel_tol, int max_iter,
   double2* Rj = g.R + (int64_t)j * ldr;
   double2* Hj = g.Hraw + (int64_t)j * ldr;
   for (int i = 0; i <= j; ++i) {
-    const double2 h = cadd(g.h1[i], g.h2[i]);
+    const double2 h = cadd(ld_cg(g.h1 + i), ld_cg(g.h2 + i));
     Rj[i] = h;
     Hj[i] = h;
   }
-  const double hn = sqrt(g.hn2[0].x);
+  const double hn = sqrt(ld_cg(g.hn2).x);
   Hj[j + 1] = make_double2(hn, 0.0);
-  // previous rotations
   for (int i = 0; i < j; ++i) {
     const double c = g.cs[i];
     const double2 s = g.sn[i];
     const double2 a = Rj[i], b = Rj[i + 1];
     Rj[i] = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
-    const double2 sc = make_double2(-s.x, s.y);  // -conj(s)
-    Rj[i + 1] = cadd(cmul(sc, a), make_double2(c * b.x, c * b.y));
+    Rj[i + 1] = cadd(cmul(make_double2(-s.x, s.y), a), make_double2(c * b.x, c * b.y));
   }
-  // new rotation zeroing hn below Rj[j]
+  // rotation zeroing hn below Rj[j]:  [c s; -conj(s) c] [a; hn] = [r; 0]
   const double2 a = Rj[j];
   const double aa = sqrt(cabs2(a));
   double c;
   double2 s, rr;
-  if (aa == 0.0) {
+  if (aa == 0.0 && hn == 0.0) {
+    c = 1.0;
+    s = make_double2(0.0, 0.0);
+    rr = make_double2(0.0, 0.0);
+  } else if (aa == 0.0) {
     c = 0.0;
     s = make_double2(1.0, 0.0);
     rr = make_double2(hn, 0.0);
@@ -226,11 +161,6 @@ __global__ void k_givens(GmresDev g, int j, double rel_tol, int max_iter,
     c = aa / r;
     s = make_double2(ph.x * hn / r, ph.y * hn / r);
     rr = make_double2(ph.x * r, ph.y * r);
-  }
-  if (aa == 0.0 && hn == 0.0) {
-    c = 1.0;
-    s = make_double2(0.0, 0.0);
-    rr = make_double2(0.0, 0.0);
   }
   g.cs[j] = c;
   g.sn[j] = s;
@@ -246,55 +176,175 @@ __global__ void k_givens(GmresDev g, int j, double rel_tol, int max_iter,
   st->iterations = k;
   st->rel = rel;
   st->hn = hn;
-  const bool breakdown = hn <= BREAKDOWN_REL * beta;
+  const bool breakdown = hn <= BREAKDOWN_REL * beta;  // solver.py:265
   st->breakdown = breakdown ? 1 : 0;
   st->inv_hn = breakdown ? 0.0 : 1.0 / hn;
   if (breakdown) {
     st->converged = 1;
-    st->flag = 1;  // breakdown
+    st->flag = 1;
     st->stop = 1;
-    return;
-  }
-  if (rel <= rel_tol) {
+  } else if (rel <= rel_tol) {  // solver.py:279
     st->converged = 1;
     st->flag = 0;
     st->stop = 1;
-    return;
-  }
-  if (k > STAG_WINDOW) {
-    const double old = g.hist[k - 1 - STAG_WINDOW];
-    if (old > 0.0 && 1.0 - rel / old < STAG_IMPROVEMENT) {
-      st->flag = 2;  // stagnation
-      st->stop = 1;
-      return;
-    }
-  }
-  if (k >= max_iter) {
-    st->flag = 3;  // maxiter
+  } else if (k > STAG_WINDOW &&  // solver.py:282-287
+             g.hist[k - 1 - STAG_WINDOW] > 0.0 &&
+             1.0 - rel / g.hist[k - 1 - STAG_WINDOW] < STAG_IMPROVEMENT) {
+    st->flag = 2;
     st->stop = 1;
+  } else if (k >= max_iter) {  // for/else, solver.py:288-289
+    st->flag = 3;
+    st->stop = 1;
+  }
+  __threadfence();
+}
+
+// ---- kernels -----------------------------------------------------------------
+
+__global__ void __launch_bounds__(RED_THREADS) k_h1(GmresDev g) {
+  if (stopped(g.st)) return;
+  const int j = g.st->iterations;
+  const double2* w = g.V + (int64_t)(j + 1) * g.n;
+  int64_t lo, hi;
+  block_range(g.n, lo, hi);
+  int bad = 0;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
+    const double2 v = ld_cg(w + e);
+    bad |= !(isfinite(v.x) && isfinite(v.y));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(g.nonfinite, 1);
+  dots_pass(g.V, g.n, j + 1, w, lo, hi, g.P + (int64_t)blockIdx.x * g.ldp);
+  if (last_block(g.ticket + 0)) {
+    reduce_partials(g.P, g.ldp, j + 1, g.h1);
+    if (threadIdx.x == 0) g.ticket[0] = 0;
   }
 }
 
-// R y = g[0:k] (upper triangular k x k); a zero pivot gives y_i = 0
-__global__ void k_backsolve(GmresDev g, int k) {
+__global__ void __launch_bounds__(RED_THREADS) k_h2(GmresDev g) {
+  if (stopped(g.st)) return;
+  const int j = g.st->iterations;
+  extern __shared__ double2 hs[];
+  const int nc = j + 1;
+  for (int i = threadIdx.x; i < nc; i += RED_THREADS) hs[i] = ld_cg(g.h1 + i);
+  __syncthreads();
+  double2* w = g.V + (int64_t)(j + 1) * g.n;
+  int64_t lo, hi;
+  block_range(g.n, lo, hi);
+  update_pass(g.V, g.n, nc, hs, w, lo, hi);
+  dots_pass(g.V, g.n, nc, w, lo, hi, g.P + (int64_t)blockIdx.x * g.ldp);
+  if (last_block(g.ticket + 1)) {
+    reduce_partials(g.P, g.ldp, nc, g.h2);
+    if (threadIdx.x == 0) g.ticket[1] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_norm_givens(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle cond) {
+  if (stopped(g.st)) return;
+  const int j = g.st->iterations;
+  extern __shared__ double2 hs[];
+  const int nc = j + 1;
+  for (int i = threadIdx.x; i < nc; i += RED_THREADS) hs[i] = ld_cg(g.h2 + i);
+  __syncthreads();
+  double2* w = g.V + (int64_t)(j + 1) * g.n;
+  int64_t lo, hi;
+  block_range(g.n, lo, hi);
+  update_pass(g.V, g.n, nc, hs, w, lo, hi);
+  norm_pass(w, lo, hi, g.P + (int64_t)blockIdx.x * g.ldp);
+  if (last_block(g.ticket + 2)) {
+    reduce_partials(g.P, g.ldp, 1, g.hn2);
+    __syncthreads();
+    __threadfence_block();
+    if (threadIdx.x == 0) {
+      g.ticket[2] = 0;
+      givens_update(g, j, rel_tol, max_iter);
+      if (cond) cudaGraphSetConditional(cond, g.st->stop ? 0u : 1u);
+    }
+  }
+}
+
+// v_{j+1} = w / ||w||; skipped once the solve stopped (column k is unused)
+__global__ void k_normalize(GmresDev g) {
+  const DevStatus* st = g.st;
+  if (stopped(st)) return;
+  const double s = st->inv_hn;
+  double2* w = g.V + (int64_t)st->iterations * g.n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = ld_cg(w + e);
+    v.x *= s;
+    v.y *= s;
+    st_cg(w + e, v);
+  }
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_begin_norm(GmresDev g, cudaGraphConditionalHandle cond) {
+  int64_t lo, hi;
+  block_range(g.n, lo, hi);
+  norm_pass(g.V, lo, hi, g.P + (int64_t)blockIdx.x * g.ldp);
+  if (last_block(g.ticket + 0)) {
+    reduce_partials(g.P, g.ldp, 1, g.hn2);
+    __syncthreads();
+    __threadfence_block();
+    if (threadIdx.x == 0) {
+      g.ticket[0] = 0;
+      DevStatus* st = g.st;
+      const double beta = sqrt(ld_cg(g.hn2).x);
+      st->iterations = 0;
+      st->flag = 0;
+      st->converged = 0;
+      st->nonfinite = 0;
+      st->breakdown = 0;
+      st->rel = 1.0;
+      st->beta = beta;
+      st->inv_hn = beta > 0.0 ? 1.0 / beta : 0.0;
+      st->hn = beta;
+      *g.nonfinite = 0;
+      for (int i = 0; i <= g.max_iter; ++i) g.g[i] = make_double2(0.0, 0.0);
+      g.g[0] = make_double2(beta, 0.0);
+      // beta == 0: x = 0, converged (solver.py:239-242)
+      st->converged = beta == 0.0 ? 1 : 0;
+      st->stop = beta == 0.0 ? 1 : 0;
+      __threadfence();
+      if (cond) cudaGraphSetConditional(cond, beta == 0.0 ? 0u : 1u);
+    }
+  }
+}
+
+__global__ void k_begin_scale(GmresDev g) {
+  const double s = g.st->inv_hn;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = ld_cg(g.V + e);
+    v.x *= s;
+    v.y *= s;
+    st_cg(g.V + e, v);
+  }
+}
+
+// R y = g[0:k] (upper triangular k x k, k = iterations); a zero pivot gives y_i = 0
+__global__ void k_backsolve(GmresDev g) {
+  const int k = g.st->iterations;
   const int ldr = g.max_iter + 1;
   for (int i = k - 1; i >= 0; --i) {
     double2 acc = g.g[i];
     for (int l = i + 1; l < k; ++l) acc = csub(acc, cmul(g.R[(int64_t)l * ldr + i], g.y[l]));
     const double2 d = g.R[(int64_t)i * ldr + i];
     const double dd = cabs2(d);
-    if (dd == 0.0) {
-      g.y[i] = make_double2(0.0, 0.0);
-    } else {
-      // acc / d
-      g.y[i] = make_double2((acc.x * d.x + acc.y * d.y) / dd, (acc.y * d.x - acc.x * d.y) / dd);
-    }
+    g.y[i] = dd == 0.0 ? make_double2(0.0, 0.0)
+                       : make_double2((acc.x * d.x + acc.y * d.y) / dd,
+                                      (acc.y * d.x - acc.x * d.y) / dd);
   }
 }
 
-__global__ void k_combine(const double2* V, int64_t ldv, int k, const double2* y, double2* x,
-                          int64_t n) {
+// x = V[:, :k] y
+__global__ void k_combine(GmresDev g, double2* x) {
   extern __shared__ double2 ys[];
+  const int k = g.st->iterations;
+  const double2* V = g.V;
+  const double2* y = g.y;
+  const int64_t ldv = g.n, n = g.n;
   for (int i = threadIdx.x; i < k; i += blockDim.x) ys[i] = y[i];
   __syncthreads();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -306,10 +356,10 @@ __global__ void k_combine(const double2* V, int64_t ldv, int k, const double2* y
 }
 
 __global__ void __launch_bounds__(RED_THREADS)
-k_resid(const double2* b, const double2* ax, int64_t n, double2* P, int ldp) {
+k_resid(GmresDev g, const double2* b, const double2* ax) {
   __shared__ double2 red[RED_THREADS / 32][RED_CHUNK];
   int64_t lo, hi;
-  block_range(n, lo, hi);
+  block_range(g.n, lo, hi);
   double2 acc[RED_CHUNK];
 #pragma unroll
   for (int u = 0; u < RED_CHUNK; ++u) acc[u] = make_double2(0.0, 0.0);
@@ -321,17 +371,19 @@ k_resid(const double2* b, const double2* ax, int64_t n, double2* P, int ldp) {
     acc[1].x = fma(bv.x, bv.x, acc[1].x);
     acc[1].x = fma(bv.y, bv.y, acc[1].x);
   }
-  block_sum_chunk(acc, red, P + (int64_t)blockIdx.x * ldp, 2);
-}
-
-__global__ void k_resid_finish(const double2* P, int ldp, DevStatus* st) {
-  double a = 0.0, b = 0.0;
-  for (int i = 0; i < RED_BLOCKS; ++i) {
-    a += P[(int64_t)i * ldp].x;
-    b += P[(int64_t)i * ldp + 1].x;
+  block_sum_chunk(acc, red, g.P + (int64_t)blockIdx.x * g.ldp, 2);
+  if (last_block(g.ticket + 0)) {
+    if (threadIdx.x == 0) {
+      g.ticket[0] = 0;
+      double a = 0.0, c = 0.0;
+      for (int i = 0; i < RED_BLOCKS; ++i) {
+        a += ld_cg(g.P + (int64_t)i * g.ldp).x;
+        c += ld_cg(g.P + (int64_t)i * g.ldp + 1).x;
+      }
+      g.st->true_num2 = a;
+      g.st->b_norm2 = c;
+    }
   }
-  st->true_num2 = a;
-  st->b_norm2 = b;
 }
 
 __global__ void k_zero(double2* x, int64_t n) {
@@ -347,62 +399,38 @@ int grid_for(int64_t n) {
 
 }  // namespace
 
-void gm_dots(const double2* V, int64_t ldv, int ncols, const double2* w, int64_t n, double2* P,
-             int ldp, int* nonfinite, cudaStream_t s) {
+void gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
+                     cudaGraphConditionalHandle cond, cudaStream_t s) {
+  const size_t hs = (size_t)(g.max_iter + 1) * sizeof(double2);
   count_launch();
-  k_dots<<<RED_BLOCKS, RED_THREADS, 0, s>>>(V, ldv, ncols, w, n, P, ldp, nonfinite);
-}
-void gm_reduce(const double2* P, int ldp, int ncols, double2* out, cudaStream_t s) {
+  k_h1<<<RED_BLOCKS, RED_THREADS, 0, s>>>(g);
   count_launch();
-  k_reduce<<<1, 128, 0, s>>>(P, ldp, ncols, out);
-}
-void gm_update_dots(const double2* V, int64_t ldv, int ncols, const double2* h, double2* w,
-                    int64_t n, double2* P, int ldp, cudaStream_t s) {
+  k_h2<<<RED_BLOCKS, RED_THREADS, hs, s>>>(g);
   count_launch();
-  k_update_dots<<<RED_BLOCKS, RED_THREADS, ncols * sizeof(double2), s>>>(V, ldv, ncols, h, w, n,
-                                                                         P, ldp);
-}
-void gm_update_norm(const double2* V, int64_t ldv, int ncols, const double2* h, double2* w,
-                    int64_t n, double2* P, int ldp, cudaStream_t s) {
+  k_norm_givens<<<RED_BLOCKS, RED_THREADS, hs, s>>>(g, rel_tol, max_iter, cond);
   count_launch();
-  k_update_norm<<<RED_BLOCKS, RED_THREADS, ncols * sizeof(double2), s>>>(V, ldv, ncols, h, w, n,
-                                                                         P, ldp);
+  k_normalize<<<grid_for(g.n), 256, 0, s>>>(g);
 }
-void gm_norm(const double2* w, int64_t n, double2* P, int ldp, int* nonfinite, cudaStream_t s) {
+
+void gm_begin(const GmresDev& g, cudaGraphConditionalHandle cond, cudaStream_t s) {
   count_launch();
-  k_norm<<<RED_BLOCKS, RED_THREADS, 0, s>>>(w, n, P, ldp, nonfinite);
-}
-void gm_begin(const GmresDev& g, cudaStream_t s) {
+  k_begin_norm<<<RED_BLOCKS, RED_THREADS, 0, s>>>(g, cond);
   count_launch();
-  k_begin<<<1, 1, 0, s>>>(g);
+  k_begin_scale<<<grid_for(g.n), 256, 0, s>>>(g);
 }
-void gm_scale(double2* w, int64_t n, const DevStatus* st, int, cudaStream_t s) {
+
+void gm_finish(const GmresDev& g, double2* x, cudaStream_t s) {
   count_launch();
-  k_scale<<<grid_for(n), 256, 0, s>>>(w, n, st);
-}
-void gm_givens(const GmresDev& g, int j, double rel_tol, int max_iter, const int* nonfinite,
-               cudaStream_t s) {
+  k_backsolve<<<1, 1, 0, s>>>(g);
   count_launch();
-  k_givens<<<1, 1, 0, s>>>(g, j, rel_tol, max_iter, nonfinite);
+  k_combine<<<grid_for(g.n), 256, (size_t)(g.max_iter + 1) * sizeof(double2), s>>>(g, x);
 }
-void gm_backsolve(const GmresDev& g, int k, cudaStream_t s) {
+
+void gm_resid(const GmresDev& g, const double2* b, const double2* ax, cudaStream_t s) {
   count_launch();
-  k_backsolve<<<1, 1, 0, s>>>(g, k);
+  k_resid<<<RED_BLOCKS, RED_THREADS, 0, s>>>(g, b, ax);
 }
-void gm_combine(const double2* V, int64_t ldv, int k, const double2* y, double2* x, int64_t n,
-                cudaStream_t s) {
-  count_launch();
-  k_combine<<<grid_for(n), 256, (k > 0 ? k : 1) * sizeof(double2), s>>>(V, ldv, k, y, x, n);
-}
-void gm_resid(const double2* b, const double2* ax, int64_t n, double2* P, int ldp,
-              cudaStream_t s) {
-  count_launch();
-  k_resid<<<RED_BLOCKS, RED_THREADS, 0, s>>>(b, ax, n, P, ldp);
-}
-void gm_resid_finish(const GmresDev& g, cudaStream_t s) {
-  count_launch();
-  k_resid_finish<<<1, 1, 0, s>>>(g.P, g.ldp, g.st);
-}
+
 void gm_zero(double2* x, int64_t n, cudaStream_t s) {
   count_launch();
   k_zero<<<grid_for(n), 256, 0, s>>>(x, n);

@@ -46,27 +46,26 @@ struct GmresDev {
   double* hist;       // residual history
   double2* y;         // least-squares solution
   DevStatus* st;
+  int* ticket;        // last-block tickets of the fused reductions (3)
+  int* nonfinite;
 };
 
-// launch helpers (pt_gmres.cu); all stream-ordered, no host sync
-void gm_dots(const double2* V, int64_t ldv, int ncols, const double2* w, int64_t n,
-             double2* P, int ldp, int* nonfinite, cudaStream_t s);
-void gm_reduce(const double2* P, int ldp, int ncols, double2* out, cudaStream_t s);
-void gm_update_dots(const double2* V, int64_t ldv, int ncols, const double2* h, double2* w,
-                    int64_t n, double2* P, int ldp, cudaStream_t s);
-void gm_update_norm(const double2* V, int64_t ldv, int ncols, const double2* h, double2* w,
-                    int64_t n, double2* P, int ldp, cudaStream_t s);
-void gm_norm(const double2* w, int64_t n, double2* P, int ldp, int* nonfinite, cudaStream_t s);
-void gm_begin(const GmresDev& g, cudaStream_t s);            // beta from hn2, g = beta e1
-void gm_scale(double2* w, int64_t n, const DevStatus* st, int use_beta, cudaStream_t s);
-void gm_givens(const GmresDev& g, int j, double rel_tol, int max_iter, const int* nonfinite,
-               cudaStream_t s);
-void gm_backsolve(const GmresDev& g, int k, cudaStream_t s);
-void gm_combine(const double2* V, int64_t ldv, int k, const double2* y, double2* x, int64_t n,
-                cudaStream_t s);
-void gm_resid(const double2* b, const double2* ax, int64_t n, double2* P, int ldp,
-              cudaStream_t s);
-void gm_resid_finish(const GmresDev& g, cudaStream_t s);
+// launch helpers (pt_gmres.cu); all stream-ordered and graph-capturable.
+// The iteration index j is read on the device (st->iterations), and every
+// iteration kernel returns at once when st->stop is set, so the same
+// kernels serve the per-step API, a speculative host loop and the CUDA
+// graph whose conditional WHILE node runs the whole loop on the device
+// (cond != 0: the kernels set the loop condition).
+// One Arnoldi step (w = basis column j+1):
+//   h1 = V^H w (+ non-finite check) | w -= V h1, h2 = V^H w |
+//   w -= V h2, ||w||, Givens + flags | w /= ||w||
+void gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
+                     cudaGraphConditionalHandle cond, cudaStream_t s);
+// ||V0||, beta, g = beta e1, V0 /= beta; stop if beta == 0
+void gm_begin(const GmresDev& g, cudaGraphConditionalHandle cond, cudaStream_t s);
+// y = R^-1 g, x = V[:, :k] y (k = st->iterations)
+void gm_finish(const GmresDev& g, double2* x, cudaStream_t s);
+void gm_resid(const GmresDev& g, const double2* b, const double2* ax, cudaStream_t s);
 void gm_zero(double2* x, int64_t n, cudaStream_t s);
 
 }  // namespace pt

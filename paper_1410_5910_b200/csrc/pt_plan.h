@@ -29,9 +29,8 @@ struct Operator {
   std::vector<DevLeaf> leaves;
   std::vector<DevSlot> slots;
   std::vector<DevKernelPLR> kplr;
-  std::vector<int32_t> rowseg;
-  std::vector<DevSegment> segs;
-  std::vector<int32_t> seg_leaves;
+  std::vector<int32_t> tile_ptr;
+  std::vector<int32_t> tile_leaves;
   std::vector<int32_t> nslot;  // per kernel: sum of ranks
 };
 
@@ -56,8 +55,8 @@ std::string sweep_diagonal_error(const Operator& op);
 // Program kinds.
 struct PlanParams {
   int dense_rows_per_task = 16;  // Y_DENSE rows per task
-  int plr_rows_per_task = 128;   // Y_PLR rows per task (thread per row)
-  int plr_slots_per_task = 32;   // T_PLR slots per task (warp per slot)
+  int plr_rows_per_task = PLR_TILE;  // Y_PLR rows per task (lane per row)
+  int plr_slots_per_task = 64;   // T_PLR slots per task (warp per slot)
 };
 
 Program build_apply_A(const Operator& op, const PlanParams& pp);

@@ -87,15 +87,13 @@ struct DevSlot {     // one Vt row, for the t-phase
   int32_t col_off, cols;
 };
 
+constexpr int PLR_TILE = 32;  // rows of a Y_PLR task (one per lane)
+
 struct DevKernelPLR {
   int32_t leaf0, nleaf;      // into the leaf table
   int32_t slot0, nslot;      // into the slot table (nslot = sum of ranks)
-  int32_t seg0;              // row -> segment map at rowseg[seg0 + row]
-  int32_t pad;
-};
-
-struct DevSegment {          // a row band covered by a fixed leaf set
-  int32_t leaf_list0, nleaf; // into seg_leaves
+  int32_t tile0;             // leaves meeting row tile t: tile_leaves[tile_ptr[tile0+t] ..
+  int32_t pad;               //                                    tile_ptr[tile0+t+1])
 };
 
 }  // namespace pt

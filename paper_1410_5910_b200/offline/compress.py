@@ -1,0 +1,67 @@
+"""Adaptive partitioned-low-rank compression (host offline), restated.
+
+Follows the reference's quadtree (plr.py:200-236, 268-297): a block whose
+smaller side is <= 2 r_max becomes a truncated-SVD leaf keeping the singular
+values >= epsilon; otherwise it is accepted as a leaf when sigma_{r_max+1} <
+epsilon, else split floor-first into quadrants (TL, TR, BL, BR).  Leaves are
+returned in preorder -- the slot order of the reference's PLRSparseForm --
+with U carrying U*Sigma; rank-0 leaves are dropped, as to_sparse_form does.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["plr_leaves", "leaf_table"]
+
+
+def _svd_leaf(block, eps):
+    u, s, vt = np.linalg.svd(block, full_matrices=False)
+    r = int(np.count_nonzero(s >= eps))
+    return np.ascontiguousarray(u[:, :r] * s[:r]), np.ascontiguousarray(vt[:r, :])
+
+
+def plr_leaves(block, r_max, eps):
+    """[(row_off, col_off, U (rows x r), Vt (r x cols))] in preorder."""
+    block = np.asarray(block, dtype=np.complex128)
+    if block.ndim != 2 or block.size == 0:
+        raise ValueError("block must be a nonempty 2D array")
+    if r_max < 1 or not eps > 0:
+        raise ValueError("need r_max >= 1 and epsilon > 0")
+    out = []
+    stack = [(0, 0, block)]
+    while stack:
+        r0, c0, b = stack.pop()
+        m, k = b.shape
+        if min(m, k) > 2 * r_max and np.linalg.svd(b, compute_uv=False)[r_max] >= eps:
+            rs, cs = m // 2, k // 2
+            # push in reverse so the pops come out TL, TR, BL, BR (preorder)
+            stack.append((r0 + rs, c0 + cs, b[rs:, cs:]))
+            stack.append((r0 + rs, c0, b[rs:, :cs]))
+            stack.append((r0, c0 + cs, b[:rs, cs:]))
+            stack.append((r0, c0, b[:rs, :cs]))
+            continue
+        u, vt = _svd_leaf(b, eps)
+        if u.shape[1]:
+            out.append((r0, c0, u, vt))
+    return out
+
+
+def leaf_table(kernels_leaves):
+    """Pack per-kernel leaf lists into the pt_leaf table + factor array."""
+    rows, chunks, kbytes = [], [], []
+    off = 0
+    for kid, leaves in enumerate(kernels_leaves):
+        nb = 0
+        for (r0, c0, u, vt) in leaves:
+            ml, r = u.shape
+            kk = vt.shape[1]
+            rows.append((kid, r0, c0, ml, kk, r, off, off + ml * r))
+            chunks.append(u.ravel())
+            chunks.append(vt.ravel())
+            off += ml * r + r * kk
+            nb += 16 * r * (ml + kk)
+        kbytes.append(nb)
+    table = np.asarray(rows, dtype=np.int64).reshape(-1, 8)
+    factors = np.concatenate(chunks) if chunks else np.zeros(0, np.complex128)
+    return table, factors, np.asarray(kbytes, dtype=np.int64)

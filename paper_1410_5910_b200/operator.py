@@ -51,7 +51,8 @@ def load_case_arrays(path):
             if k in oarr:
                 arrays[k] = oarr[k]
         for k in ("kernel_format", "n_kernels", "kernel_bytes"):
-            meta[k] = ometa[k]
+            if k in ometa:
+                meta[k] = ometa[k]
     return meta, arrays
 
 
@@ -223,6 +224,17 @@ class DeviceOperator:
         rc = nat.lib().pt_gmres_host(self._h, bp, xp, C.byref(cfg), C.byref(rep), self.stream())
         nat.check(rc, "pt_gmres_host")
         return _report_dict(rep, hist)
+
+    def exec_timing(self, enable=True):
+        """Bracket every executor launch with CUDA events (resets the stats)."""
+        nat.check(nat.lib().pt_exec_timing(self._h, 1 if enable else 0), "pt_exec_timing")
+
+    def exec_stats(self):
+        """(device ms summed over timed launches, launches, algorithmic bytes)."""
+        ms, n, b = C.c_double(), C.c_int64(), C.c_int64()
+        nat.check(nat.lib().pt_exec_stats(self._h, C.byref(ms), C.byref(n), C.byref(b)),
+                  "pt_exec_stats")
+        return float(ms.value), int(n.value), int(b.value)
 
     def bytes_apply_A(self):
         return int(nat.lib().pt_bytes_apply_A(self._h))

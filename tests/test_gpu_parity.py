@@ -26,7 +26,13 @@ def rel(a, b):
 
 
 def get(name, big=False):
-    path = case_path(name) if big else golden_path(name)
+    if big:
+        # operators above the shipping limit are rebuilt here by the restated
+        # offline stage and verified against the reference's checksums
+        from paper_1410_5910_b200.offline.build import ensure_case
+        path = ensure_case(name)
+    else:
+        path = golden_path(name)
     if not path.exists():
         pytest.skip(f"{path} not generated")
     if name not in _OPS:
@@ -232,7 +238,8 @@ def test_large_case_parity(cuda_ok, name):
 def test_c5_batch_parity(cuda_ok):
     meta, arr, op = get("c5", big=True)
     nt, m = meta["nt"], meta["m"]
-    for s in range(0, 64, 9):
+    assert np.asarray(arr["rhs"]).shape[0] == 64
+    for i, s in enumerate(np.asarray(arr["ref_index"])):
         x, rep = op.gmres(arr["rhs"][s], rel_tol=meta["gmres_tol"])
-        assert abs(rep["iterations"] - meta["solves"][s]["iterations"]) <= 1
-        assert rel(x[: nt * m] + x[nt * m:], arr["ref_traces"][s]) <= TRACE_TOL
+        assert abs(rep["iterations"] - meta["solves"][i]["iterations"]) <= 1
+        assert rel(x[: nt * m] + x[nt * m:], arr["ref_traces"][i]) <= TRACE_TOL

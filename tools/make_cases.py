@@ -31,8 +31,6 @@ Usage::
 from __future__ import annotations
 
 import argparse
-import json
-import math
 import sys
 import time
 from pathlib import Path
@@ -61,243 +59,33 @@ from paper_1410_5910_b200.cache import write_case  # noqa: E402
 
 
 # ----------------------------------------------------------------------------
-# media and sources
+# configurations: one definition, shared with the GPU-box builder
 
 
-def interior_xz(grid):
-    x = grid.x_coords()[grid.interior_x_slice()]
-    z = grid.z_coords()[grid.interior_z_slice()]
-    return np.meshgrid(x, z)
+def config(name):
+    """The package's CaseConfig mapped onto the reference's own objects."""
+    from paper_1410_5910_b200.offline.configs import config as pkg_config
+    c = pkg_config(name)
+    g = ComplexGrid2D(nx=c.geo.nx, nz=c.geo.nz, h=c.geo.h, n_pml=c.geo.n_pml)
+    comp = None
+    if c.compression is not None:
+        comp = CompressionConfig(epsilon=c.compression[0], r_max=c.compression[1])
+    return dict(grid=g, c=c.c, L=c.L, omega=c.omega, sources=c.sources, compression=comp,
+                tol=c.tol, note=c.note)
 
 
 def model_from_c(grid, c):
     return SquaredSlownessModel.from_interior(1.0 / c**2, grid.n_pml)
 
 
-def medium_homogeneous(grid, c0=1.0):
-    return np.full((grid.nz, grid.nx), float(c0))
-
-
-def medium_gradient(grid):
-    X, Z = interior_xz(grid)
-    return 1.0 + 0.1 * X + 0.1 * Z
-
-
-def medium_bumps(grid, seed=2, count=12):
-    X, Z = interior_xz(grid)
-    rng = np.random.default_rng(seed)
-    c = np.full_like(X, 1.5)
-    for _ in range(count):
-        xk = rng.uniform(0.0, 1.0, size=2)
-        ak = rng.uniform(-0.5, 1.5)
-        wk = rng.uniform(0.05, 0.2)
-        c = c + ak * np.exp(-((X - xk[0]) ** 2 + (Z - xk[1]) ** 2) / (2 * wk**2))
-    return np.clip(c, 1.5, 4.5)
-
-
-def medium_layered(grid, seed=3, n_layers=20, amp_h=3.0):
-    X, Z = interior_xz(grid)
-    rng = np.random.default_rng(seed)
-    vel = rng.uniform(1.5, 5.5, size=n_layers)
-    count = np.zeros(X.shape, dtype=np.int64)
-    for k in range(1, n_layers):
-        kappa = rng.uniform(1.0, 4.0)
-        phi = rng.uniform(0.0, 2 * np.pi)
-        zk = k * grid.Lz / n_layers + amp_h * grid.h * np.sin(2 * np.pi * kappa * X / grid.Lx + phi)
-        count += (Z > zk).astype(np.int64)
-    return vel[count]
-
-
-def source_point(grid, fx, fz, amp=1.0):
-    f = np.zeros((grid.nz_ext, grid.nx_ext), dtype=np.complex128)
-    px = min(max(int(round(fx * (grid.nx + 1))), 1), grid.nx)
-    qz = min(max(int(round(fz * (grid.nz + 1))), 1), grid.nz)
-    f[grid.n_pml + qz - 1, grid.n_pml + px - 1] = amp / grid.h**2
-    return f
-
-
-def source_gaussian(grid, fx, fz, sigma):
-    f = np.zeros((grid.nz_ext, grid.nx_ext), dtype=np.complex128)
-    x = grid.x_coords()
-    z = grid.z_coords()[grid.interior_z_slice()]
-    X, Z = np.meshgrid(x, z)
-    x0, z0 = fx * grid.Lx, fz * grid.Lz
-    g = np.exp(-((X - x0) ** 2 + (Z - z0) ** 2) / (2 * sigma**2)) / (2 * np.pi * sigma**2)
-    f[grid.interior_z_slice(), :] = g
-    return f
-
-
-def source_random(grid, seed):
-    rng = np.random.default_rng(seed)
-    f = np.zeros((grid.nz_ext, grid.nx_ext), dtype=np.complex128)
-    shape = (grid.nz, grid.nx_ext)
-    f[grid.interior_z_slice(), :] = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
-    return f
-
-
-# ----------------------------------------------------------------------------
-# configurations
-
-
-def _grid(nx, nz, n_pml):
-    return ComplexGrid2D(nx=nx, nz=nz, h=1.0 / (nx + 1), n_pml=n_pml)
-
-
-def config(name):
-    """Return dict(grid, c, L, omega, sources, compression, tol, note)."""
-    if name == "c1":
-        g = _grid(200, 200, 20)
-        c = medium_homogeneous(g)
-        return dict(grid=g, c=c, L=4, omega=2 * np.pi * 20,
-                    sources=[("gauss", source_gaussian(g, 0.5, 0.1, 2 * g.h))],
-                    compression=None, tol=1e-9,
-                    note="homogeneous c=1, 200^2+20 PML, omega=2pi*20, L=4, Gaussian source sigma=2h, dense")
-    if name in ("c2", "c5"):
-        g = _grid(400, 400, 30)
-        c = medium_bumps(g)
-        omega = 2 * np.pi * c.min() / (10 * g.h)
-        if name == "c2":
-            src = [("point", source_point(g, 0.5, 0.1))]
-            note = "12 seeded Gaussian bumps (rng 2), 400^2+30 PML, 10 ppw, L=8, point source, dense"
-        else:
-            src = [(f"point{s}", source_point(g, (s + 0.5) / 64, 0.05)) for s in range(64)]
-            note = "c2 medium and layering, 64 point sources at depth 0.05 (multi-RHS batch)"
-        return dict(grid=g, c=c, L=8, omega=omega, sources=src, compression=None, tol=1e-9, note=note)
-    if name == "c3":
-        g = _grid(800, 800, 40)
-        c = medium_layered(g)
-        omega = 2 * np.pi * c.min() / (8 * g.h)
-        return dict(grid=g, c=c, L=16, omega=omega,
-                    sources=[("point", source_point(g, 0.5, 0.1))],
-                    compression=CompressionConfig(epsilon=1e-9, r_max=32), tol=1e-9,
-                    note="20 seeded layers (rng 3) with 3h undulation, 800^2+40 PML, 8 ppw, L=16, point source, PLR eps 1e-9 r_max 32")
-    if name == "c3r":
-        g = _grid(160, 160, 16)
-        c = medium_layered(g)
-        omega = 2 * np.pi * c.min() / (8 * g.h)
-        return dict(grid=g, c=c, L=4, omega=omega,
-                    sources=[("point", source_point(g, 0.5, 0.1))],
-                    compression=CompressionConfig(epsilon=1e-9, r_max=32), tol=1e-9,
-                    note="reduced c3: layered medium 160^2+16 PML, 8 ppw, L=4, PLR eps 1e-9 r_max 32")
-    # ---- small fixtures (tests/golden) ----
-    if name == "fx_tiny":
-        g = _grid(8, 9, 3)
-        return dict(grid=g, c=medium_gradient(g), L=3, omega=4.0,
-                    sources=[("rand", source_random(g, 7))], compression=None, tol=1e-10,
-                    note="reference test_solver.py tiny geometry: 8x9, L=3, n_pml=3, omega=4, gradient")
-    if name == "fx_l2":
-        g = _grid(12, 12, 4)
-        return dict(grid=g, c=medium_gradient(g), L=2, omega=6.0,
-                    sources=[("point", source_point(g, 0.4, 0.3))], compression=None, tol=1e-10,
-                    note="L=2 edge case (no kernel-bearing sweep steps)")
-    if name == "fx_uneven":
-        g = _grid(10, 19, 4)
-        return dict(grid=g, c=medium_gradient(g), L=4, omega=7.0,
-                    sources=[("point", source_point(g, 0.5, 0.7))], compression=None, tol=1e-10,
-                    note="uneven layers 5,5,5,4 (remainder to the front), L=4")
-    if name == "fx_plr":
-        g = _grid(40, 40, 10)
-        return dict(grid=g, c=medium_gradient(g), L=4, omega=9.0,
-                    sources=[("point", source_point(g, 0.5, 0.25))],
-                    compression=CompressionConfig(epsilon=1e-9, r_max=4), tol=1e-10,
-                    note="PLR with real quadtree splits: m=60, r_max=4 (min leaf 8), L=4")
-    if name == "fx_plr_odd":
-        g = _grid(37, 30, 8)
-        return dict(grid=g, c=medium_layered(g, seed=5, n_layers=5, amp_h=1.0), L=3, omega=11.0,
-                    sources=[("point", source_point(g, 0.3, 0.5))],
-                    compression=CompressionConfig(epsilon=1e-6, r_max=3), tol=1e-10,
-                    note="PLR with odd m=53 (floor-first splits), eps 1e-6 (rank-deficient leaves), L=3")
-    raise KeyError(name)
-
-
 # ----------------------------------------------------------------------------
 # operator capture
 
 
-def _leaves_from_sparse_form(sf):
-    """Recover quadtree leaves from the reference's PLRSparseForm (plr.py:268-297).
-
-    Slots are assigned leaf by leaf in preorder; a leaf occupies a run of
-    consecutive slots sharing one row range (in ``left``) and one column
-    range (in ``right``).  Explicit zeros are stored, so the ranges are exact.
-    """
-    left = sf.left.tocsc()
-    right = sf.right.tocsr()
-    n_slots = right.shape[0]
-    spans = []
-    for s in range(n_slots):
-        rows = left.indices[left.indptr[s]:left.indptr[s + 1]]
-        cols = right.indices[right.indptr[s]:right.indptr[s + 1]]
-        spans.append((int(rows.min()), int(rows.max()) + 1, int(cols.min()), int(cols.max()) + 1))
-    leaves = []
-    s = 0
-    while s < n_slots:
-        e = s + 1
-        while e < n_slots and spans[e] == spans[s]:
-            e += 1
-        r0, r1, c0, c1 = spans[s]
-        assert left.indptr[s + 1] - left.indptr[s] == r1 - r0
-        assert right.indptr[s + 1] - right.indptr[s] == c1 - c0
-        u = sf.left[r0:r1, s:e].toarray()
-        vt = sf.right[s:e, c0:c1].toarray()
-        leaves.append((r0, c0, u, vt))
-        s = e
-    return leaves
-
-
 def capture_operator(state):
-    pol = state.pol
-    m = pol.m
-    items = sorted(pol.entries.items())
-    kid = {}
-    kernels = []
-    entries = np.zeros((len(items), 3), dtype=np.int64)
-    coefs = np.zeros((len(items), 2), dtype=np.complex128)
-    for n, ((i, j), e) in enumerate(items):
-        k = -1
-        if e.kernel is not None:
-            key = id(e.kernel)
-            if key not in kid:
-                kid[key] = len(kernels)
-                kernels.append(e.kernel)
-            k = kid[key]
-        entries[n] = (i, j, k)
-        coefs[n] = (e.scale, e.eye)
-    arrays = {"entries": entries, "coefs": coefs, "perm": np.asarray(state.perm, dtype=np.int64)}
-    if all(isinstance(k, np.ndarray) for k in kernels):
-        arrays["dense"] = np.stack([np.asarray(k, dtype=np.complex128) for k in kernels])
-        fmt = "dense"
-        kbytes = [16 * m * m] * len(kernels)
-    else:
-        fmt = "plr"
-        leaf_rows, chunks, kl = [], [], []
-        off = 0
-        kbytes = []
-        for k_id, sf in enumerate(kernels):
-            leaves = _leaves_from_sparse_form(sf)
-            kl.append((len(leaf_rows), len(leaves)))
-            nb = 0
-            for (r0, c0, u, vt) in leaves:
-                ml, r = u.shape
-                kk = vt.shape[1]
-                leaf_rows.append((k_id, r0, c0, ml, kk, r, off, off + ml * r))
-                chunks.append(np.ascontiguousarray(u).ravel())
-                chunks.append(np.ascontiguousarray(vt).ravel())
-                off += ml * r + r * kk
-                nb += 16 * r * (ml + kk)
-            assert nb == 16 * sf.stored_entries(), (nb, sf.stored_entries())
-            kbytes.append(nb)
-            # the recovered leaves must reproduce the reference factor product
-            dense = np.zeros((m, m), dtype=np.complex128)
-            for (r0, c0, u, vt) in leaves:
-                dense[r0:r0 + u.shape[0], c0:c0 + vt.shape[1]] += u @ vt
-            ref = sf.to_dense()
-            scale = max(np.abs(ref).max(), 1e-300)
-            assert np.abs(dense - ref).max() <= 1e-12 * scale
-        arrays["leaves"] = np.asarray(leaf_rows, dtype=np.int64).reshape(-1, 8)
-        arrays["kernel_leaves"] = np.asarray(kl, dtype=np.int64).reshape(-1, 2)
-        arrays["factors"] = np.concatenate(chunks) if chunks else np.zeros(0, np.complex128)
-    return fmt, arrays, kbytes
+    from paper_1410_5910_b200.capture import capture_operator as cap
+    meta, arrays = cap(state.pol, state.perm)
+    return meta["kernel_format"], arrays, list(arrays["kernel_bytes"])
 
 
 # ----------------------------------------------------------------------------
@@ -344,7 +132,6 @@ def build(name, out_dir, operator_from=None, state_cache={}):
         meta["n_kernels"] = len(kbytes)
         meta["kernel_bytes"] = int(sum(kbytes))
         arrays.update(op_arrays)
-        arrays["kernel_bytes"] = np.asarray(kbytes, dtype=np.int64)
 
     # probe applies on seeded vectors (per-apply parity targets)
     rng = np.random.default_rng(1234)
@@ -411,20 +198,59 @@ def build(name, out_dir, operator_from=None, state_cache={}):
 
 
 FIXTURES = ["fx_tiny", "fx_l2", "fx_uneven", "fx_plr", "fx_plr_odd"]
+LITE_SUBSET = {"c5": list(range(0, 64, 9))}
+
+
+def write_lite(name, full_dir=ROOT / "cases", out_dir=ROOT / "tests" / "golden"):
+    """tests/golden/<name>_ref.ptc: the reference's results and operator
+    checksums for a large case, without the kernels (which exceed what can be
+    shipped to the GPU box; the box rebuilds them with
+    paper_1410_5910_b200.offline.build and verifies them against these
+    checksums)."""
+    from paper_1410_5910_b200.cache import read_case
+    from paper_1410_5910_b200.offline.build import operator_checksums
+    from paper_1410_5910_b200.operator import load_case_arrays
+    meta, arr = load_case_arrays(Path(full_dir) / f"{name}.ptc")
+    ck = operator_checksums(meta, arr)
+    idx = LITE_SUBSET.get(name, list(range(arr["rhs"].shape[0])))
+    lite = dict(ck)
+    lite["ref_index"] = np.asarray(idx, dtype=np.int64)
+    for k in ("rhs", "ref_x", "ref_traces", "ref_hist"):
+        lite[k] = np.asarray(arr[k])[idx]
+    for k in ("probe_x", "probe_u", "probe_Ax", "probe_Mx", "probe_M1x", "probe_sweep"):
+        lite[k] = np.asarray(arr[k])
+    lmeta = {k: meta[k] for k in ("name", "note", "nx", "nz", "n_pml", "h", "L", "n_c", "omega",
+                                  "m", "nt", "N", "c_min", "c_max", "gmres_tol", "gmres_max_iter",
+                                  "n_it", "offline_seconds", "offline_stage_seconds",
+                                  "probe_apply_seconds", "generator") if k in meta}
+    lmeta["solves"] = [meta["solves"][i] for i in idx]
+    lmeta["kernel_format"] = meta.get("kernel_format")
+    lmeta["kernel_bytes"] = meta.get("kernel_bytes")
+    out = Path(out_dir) / f"{name}_ref.ptc"
+    write_case(out, lmeta, lite)
+    print(f"[{name}] lite golden {out} ({out.stat().st_size / 1e6:.2f} MB)", flush=True)
+    return out
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("names", nargs="+")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--lite", action="store_true",
+                    help="only write tests/golden/<name>_ref.ptc from an existing cases/<name>.ptc")
     args = ap.parse_args(argv)
     names = []
     for n in args.names:
         names += FIXTURES if n == "fixtures" else [n]
     for n in names:
+        if args.lite:
+            write_lite(n)
+            continue
         out = args.out or (ROOT / "tests" / "golden" if n.startswith("fx_") else ROOT / "cases")
         Path(out).mkdir(parents=True, exist_ok=True)
         build(n, out)
+        if not n.startswith("fx_"):
+            write_lite(n)
 
 
 if __name__ == "__main__":
