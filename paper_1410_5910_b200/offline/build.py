@@ -254,7 +254,7 @@ def main(argv=None):
         print(json.dumps({"case": n, "path": str(p), "seconds": round(time.perf_counter() - t, 1),
                           "offline_stage_seconds": m["offline_stage_seconds"],
                           "verified": m.get("verified_against_reference", False),
-                          "kernel_bytes": m["kernel_bytes"]}), flush=True)
+                          "kernel_bytes": m.get("kernel_bytes")}), flush=True)
 
 
 if __name__ == "__main__":
