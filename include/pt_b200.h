@@ -170,6 +170,14 @@ int pt_exec_timing(pt_handle *h, int32_t enable);
 int pt_exec_stats(pt_handle *h, double *total_ms, int64_t *launches,
                   int64_t *algo_bytes);
 
+/* Run one operator program (kind 0 = A-apply, 1 = n_it-sweep preconditioner,
+ * 2 = fused A->M iteration, 3 = one sweep with u_in = in) with a per-task
+ * timeline: rec[12*q ...] = {type, out slot, out offset, r0, r1, terms,
+ * t_grab, t_ready, t_done (globaltimer ns), SM id, kernel (T tasks), group}
+ * for every task q in queue order.  Profiling aid; synchronises. */
+int pt_trace_program(pt_handle *h, int32_t kind, int32_t n_it, const double *in,
+                     double *out, int64_t *rec, int64_t cap, int64_t *n_out);
+
 /* ---- misc ----------------------------------------------------------------*/
 const char *pt_last_error(void);
 int32_t pt_abi_version(void);

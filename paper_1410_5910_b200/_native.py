@@ -70,6 +70,8 @@ _SIGS = {
     "pt_exec_timing": (C.c_int, [_VP, C.c_int32]),
     "pt_exec_stats": (C.c_int, [_VP, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64)]),
+    "pt_trace_program": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP, C.POINTER(C.c_int64),
+                                   C.c_int64, C.POINTER(C.c_int64)]),
     "pt_last_error": (C.c_char_p, []),
     "pt_abi_version": (C.c_int32, []),
     "pt_launch_count": (C.c_int64, []),

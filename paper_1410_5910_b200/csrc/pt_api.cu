@@ -54,7 +54,9 @@ struct DevProgram {
   DevTerm* terms = nullptr;
   DevEye* eyes = nullptr;
   DevWait* waits = nullptr;
+  DevTileEntry* ents = nullptr;
   ~DevProgram() {
+    cudaFree(ents);
     cudaFree(tasks);
     cudaFree(terms);
     cudaFree(eyes);
@@ -113,7 +115,7 @@ struct pt_handle {
   DevSlot* slots = nullptr;
   DevKernelPLR* kplr = nullptr;
   int32_t* tile_ptr = nullptr;
-  int32_t* tile_leaves = nullptr;
+  DevTileEntry* tile_ent = nullptr;
   std::map<std::string, std::unique_ptr<DevProgram>> progs;
   double2* slot_buf[N_SLOTS] = {nullptr};
   int64_t slot_cap[N_SLOTS] = {0};
@@ -140,6 +142,8 @@ struct pt_handle {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     graphs.clear();
   }
+  // per-task timeline of one traced launch (pt_trace_program)
+  unsigned long long* trace_buf = nullptr;
   // per-launch instrumentation of the executor
   bool timing = false;
   std::vector<cudaEvent_t> ev_free;
@@ -163,7 +167,7 @@ struct pt_handle {
     cudaFree(slots);
     cudaFree(kplr);
     cudaFree(tile_ptr);
-    cudaFree(tile_leaves);
+    cudaFree(tile_ent);
     for (int s = 0; s < N_SLOTS; ++s) cudaFree(slot_buf[s]);
     cudaFree(ctr);
     cudaFree(tmp);
@@ -247,16 +251,26 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
     const int64_t ntiles = (m + PLR_TILE - 1) / PLR_TILE;
     kp.tile0 = (int32_t)op.tile_ptr.size();
     for (int64_t t = 0; t < ntiles; ++t) {
-      op.tile_ptr.push_back((int32_t)op.tile_leaves.size());
+      op.tile_ptr.push_back((int32_t)op.tile_ent.size());
       const int64_t lo = t * PLR_TILE, hi = std::min<int64_t>(m, lo + PLR_TILE);
       for (int32_t l = kp.leaf0; l < kp.leaf0 + kp.nleaf; ++l) {
         const DevLeaf& dl = op.leaves[l];
-        if (dl.row_off < hi && dl.row_off + dl.rows > lo) op.tile_leaves.push_back(l);
+        if (!(dl.row_off < hi && dl.row_off + dl.rows > lo)) continue;
+        DevTileEntry te{};
+        const int64_t r_first = std::max<int64_t>(lo, dl.row_off);
+        const int64_t r_end = std::min<int64_t>(hi, dl.row_off + dl.rows);
+        te.u0 = dl.u_off + (r_first - dl.row_off);
+        te.t0 = dl.slot0;
+        te.stride = dl.rows;
+        te.rank = dl.rank;
+        te.lo = (int16_t)(r_first - lo);
+        te.hi = (int16_t)(r_end - lo);
+        op.tile_ent.push_back(te);
       }
     }
-    op.tile_ptr.push_back((int32_t)op.tile_leaves.size());
+    op.tile_ptr.push_back((int32_t)op.tile_ent.size());
   }
-  if (op.tile_leaves.empty()) op.tile_leaves.push_back(0);
+  if (op.tile_ent.empty()) op.tile_ent.push_back(DevTileEntry{});
   if (blob.empty()) blob.push_back(make_double2(0.0, 0.0));
   int rc;
   if ((rc = upload(&h->fac, blob))) return rc;
@@ -264,7 +278,7 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
   if ((rc = upload(&h->slots, op.slots))) return rc;
   if ((rc = upload(&h->kplr, op.kplr))) return rc;
   if ((rc = upload(&h->tile_ptr, op.tile_ptr))) return rc;
-  if ((rc = upload(&h->tile_leaves, op.tile_leaves))) return rc;
+  if ((rc = upload(&h->tile_ent, op.tile_ent))) return rc;
   return 0;
 }
 
@@ -296,11 +310,15 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
     p->host = build_gs_sweep(h->op, h->pp);
   else
     p->host = build_A_then_M(h->op, n_it, h->pp);
+  if (p->host.overflow)
+    return fail(PT_EINVAL, "a PLR row tile meets more leaves than the executor stages (" +
+                               std::to_string(MAX_TILE_ENTRIES) + ")");
   int rc;
   if ((rc = upload(&p->tasks, p->host.tasks))) return rc;
   if ((rc = upload(&p->terms, p->host.terms))) return rc;
   if ((rc = upload(&p->eyes, p->host.eyes))) return rc;
   if ((rc = upload(&p->waits, p->host.waits))) return rc;
+  if ((rc = upload(&p->ents, p->host.ents))) return rc;
   for (int s : {SLOT_Y, SLOT_U1, SLOT_U2, SLOT_PRE, SLOT_T})
     if ((rc = ensure_slot(h, s, p->host.slot_elems[s]))) return rc;
   if (p->host.n_counters + 1 > h->ctr_cap) {
@@ -341,13 +359,15 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.slots = h->slots;
   a.kplr = h->kplr;
   a.tile_ptr = h->tile_ptr;
-  a.tile_leaves = h->tile_leaves;
+  a.tile_ent = h->tile_ent;
+  a.ents = p->ents;
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
   a.stop = stop;
   a.iter = im.iter;
   a.vbase = im.vbase;
   a.vstride = im.vstride;
+  a.trace = h->trace_buf;
   CK(cudaMemsetAsync(h->ctr, 0, (p->host.n_counters + 1) * sizeof(int), s));
   count_launch();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -536,7 +556,9 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     if (n_leaves > 0 && (!leaves || !factors)) return fail(PT_EINVAL, "PLR tables missing");
     if ((rc = build_plr_tables(h.get(), leaves, n_leaves, factors, n_factor_complex))) return rc;
   }
-  h->smem = std::max<size_t>((size_t)op.m, EXEC_THREADS) * sizeof(double2);
+  // [source staging: m][partials: EXEC_THREADS][task metadata: MAX_TILE_ENTRIES entries]
+  h->smem = ((size_t)op.m + EXEC_THREADS) * sizeof(double2) +
+            MAX_TILE_ENTRIES * sizeof(DevTileEntry);
   if (h->smem > 48 * 1024)
     CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)h->smem));
@@ -545,8 +567,13 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_exec_kernel, EXEC_THREADS, h->smem));
   if (occ < 1) return fail(PT_EINVAL, "executor kernel does not fit on an SM");
   h->grid = nsm * occ;
+  h->pp.ctas = h->grid;
   h->pp.dense_rows_per_task = DENSE_ROWS_PER_TASK;
   h->pp.plr_rows_per_task = PLR_TILE;
+  h->pp.plr_slots_per_task = 16;
+  if (const char* e = std::getenv("PT_DENSE_ROWS"))
+    h->pp.dense_rows_per_task = std::max(1, std::min(DENSE_RT_MAX, std::atoi(e)));
+  if (const char* e = std::getenv("PT_T_SLOTS")) h->pp.plr_slots_per_task = std::max(1, std::atoi(e));
   CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
   *out = h.release();
   return 0;
@@ -929,6 +956,50 @@ int pt_exec_stats(pt_handle* h, double* total_ms, int64_t* launches, int64_t* al
   if (algo_bytes) *algo_bytes = h->timed_bytes;
   h->timed_launches = 0;
   h->timed_bytes = 0;
+  return 0;
+}
+
+int pt_trace_program(pt_handle* h, int32_t kind, int32_t n_it, const double* in, double* out,
+                     int64_t* rec, int64_t cap, int64_t* n_out) {
+  if (!h || !in || !out || !rec || !n_out) return fail(PT_EINVAL, "null argument");
+  DeviceGuard guard(h->device);
+  const char* names[] = {"A", "M", "AM", "S"};
+  if (kind < 0 || kind > 3) return fail(PT_EINVAL, "unknown program kind");
+  if (kind != 0 && !h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  DevProgram* p;
+  int rc = get_program(h, names[kind], kind == 0 || kind == 3 ? 0 : n_it, &p);
+  if (rc) return rc;
+  const int64_t nt = (int64_t)p->host.tasks.size();
+  *n_out = nt;
+  if (cap < nt) return fail(PT_EINVAL, "trace buffer too small");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMalloc(&h->trace_buf, (size_t)std::max<int64_t>(nt, 1) * 4 * sizeof(unsigned long long)));
+  rc = run_program(h, p, (const double2*)in, (double2*)out, (const double2*)in, 0);
+  std::vector<unsigned long long> tr((size_t)nt * 4);
+  cudaError_t e1 = cudaDeviceSynchronize();
+  cudaError_t e2 = cudaMemcpy(tr.data(), h->trace_buf, tr.size() * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost);
+  cudaFree(h->trace_buf);
+  h->trace_buf = nullptr;
+  if (rc) return rc;
+  CK(e1);
+  CK(e2);
+  for (int64_t q = 0; q < nt; ++q) {
+    const DevTask& t = p->host.tasks[q];
+    int64_t* r = rec + 12 * q;
+    r[0] = t.type;
+    r[1] = t.out.slot;
+    r[2] = t.out.off;
+    r[3] = t.r0;
+    r[4] = t.r1;
+    r[5] = t.nterm;
+    r[6] = (int64_t)tr[4 * q + 0];
+    r[7] = (int64_t)tr[4 * q + 1];
+    r[8] = (int64_t)tr[4 * q + 2];
+    r[9] = (int64_t)tr[4 * q + 3];
+    r[10] = t.type == TASK_T_PLR ? p->host.terms[t.term0].kernel : -1;
+    r[11] = t.signal;
+  }
   return 0;
 }
 

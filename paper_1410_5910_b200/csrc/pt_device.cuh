@@ -9,8 +9,8 @@ namespace pt {
 
 constexpr int EXEC_THREADS = 256;
 constexpr int EXEC_WARPS = EXEC_THREADS / 32;
-constexpr int DENSE_RPW = 2;  // rows per warp of a Y_DENSE task
-constexpr int DENSE_ROWS_PER_TASK = EXEC_WARPS * DENSE_RPW;
+constexpr int DENSE_RT_MAX = 4;   // max rows of a Y_DENSE task (split-K over warps)
+constexpr int DENSE_ROWS_PER_TASK = 4;
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
   return make_double2(a.x + b.x, a.y + b.y);
@@ -80,16 +80,40 @@ struct ExecArgs {
   const DevSlot* slots;
   const DevKernelPLR* kplr;
   const int32_t* tile_ptr;
-  const int32_t* tile_leaves;
+  const DevTileEntry* tile_ent;
+  const DevTileEntry* ents;  // program's Y_PLR task entries
   const int* stop;  // GMRES status stop flag: the whole launch is skipped once set
   // iteration-relative basis addressing (GMRES loop inside a graph):
   // if iter != nullptr, SLOT_IN = vbase + (*iter) * vstride, SLOT_OUT = SLOT_IN + vstride
   const int* iter;
   double2* vbase;
   int64_t vstride;
+  unsigned long long* trace;  // optional per-task timeline (debug/profiling)
   int n_tasks;
   int m;
 };
+
+// TMA bulk prefetch of a contiguous range into L2 (no smem, no completion)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  const char* c = (const char*)p;
+  while (bytes > 0) {
+    const uint32_t n = bytes > 32768u ? 32768u : bytes;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c), "r"(n) : "memory");
+    c += n;
+    bytes -= n;
+  }
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 __global__ void pt_exec_kernel(ExecArgs a);
 

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <queue>
 #include <set>
 #include <sstream>
 
@@ -117,6 +118,23 @@ class Builder {
     const int rpt = plr ? pp_.plr_rows_per_task : pp_.dense_rows_per_task;
     for (int64_t r0 = 0; r0 < m; r0 += rpt) {
       DevTask tk{};
+      if (plr) {  // flat tile entries of all terms, t0 absolute, prefix column counts
+        tk.ent0 = (int32_t)prog_.ents.size();
+        int32_t pre = 0;
+        for (size_t it = 0; it < terms.size(); ++it) {
+          const DevTerm& dt = prog_.terms[term0 + it];
+          const int32_t k0 = op_.kplr[dt.kernel].tile0 + (int32_t)(r0 / PLR_TILE);
+          for (int32_t e = op_.tile_ptr[k0]; e < op_.tile_ptr[k0 + 1]; ++e) {
+            DevTileEntry te = op_.tile_ent[e];
+            te.t0 = (int32_t)(te.t0 + dt.t_base);
+            te.pre = pre;
+            pre += te.rank;
+            prog_.ents.push_back(te);
+          }
+        }
+        tk.nent = (int32_t)prog_.ents.size() - tk.ent0;
+        if (tk.nent > MAX_TILE_ENTRIES) overflow_ = true;
+      }
       tk.type = plr ? TASK_Y_PLR : TASK_Y_DENSE;
       tk.r0 = (int32_t)r0;
       tk.r1 = (int32_t)std::min<int64_t>(m, r0 + rpt);
@@ -136,6 +154,7 @@ class Builder {
     return g;
   }
 
+  bool overflow() const { return overflow_; }
   void begin_stage() { sweep_kernels_.clear(); }
   void end_stage() {
     for (int64_t k : sweep_kernels_) prog_.algo_bytes += op_.kernel_bytes[k];
@@ -148,30 +167,67 @@ class Builder {
 
   Program finish() {
     const int n = (int)prog_.tasks.size();
-    // depth = longest path from a root (topological levels)
-    std::vector<int> depth(n, 0), gdepth(groups_.size(), -1);
-    for (int t = 0; t < n; ++t) {
-      int d = 0;
-      for (int g : task_waits_[t]) d = std::max(d, gdepth[g] + 1);
-      depth[t] = d;
-      int& gd = gdepth[task_group_[t]];
-      gd = std::max(gd, d);
-    }
-    // bottom level = cost-weighted longest path to a sink
+    // modelled duration of each task on one CTA
+    std::vector<double> dur(n);
+    for (int t = 0; t < n; ++t) dur[t] = pp_.task_us + task_cost_[t] / (pp_.cta_gbs * 1e3);
+    // bottom level = duration-weighted longest path to a sink (priority)
     std::vector<double> bl(n, 0.0), gcons(groups_.size(), 0.0);
     for (int t = n - 1; t >= 0; --t) {
-      bl[t] = task_cost_[t] + gcons[task_group_[t]];
+      bl[t] = dur[t] + gcons[task_group_[t]];
       for (int g : task_waits_[t]) gcons[g] = std::max(gcons[g], bl[t]);
     }
-    std::vector<int> order(n);
-    for (int t = 0; t < n; ++t) order[t] = t;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      if (depth[a] != depth[b]) return depth[a] < depth[b];
-      return bl[a] > bl[b];
-    });
+    // List-scheduling simulation on pp_.ctas CTAs: a task is released when
+    // all its producer groups have finished; a free CTA takes the released
+    // task with the longest remaining path.  The queue order is the
+    // simulated start order, so CTAs grabbing in queue order interleave
+    // independent groups the way the schedule does (topological by
+    // construction: a task starts after its producers finish).
+    std::vector<int> unmet(n), gleft(groups_.size(), 0);
+    std::vector<std::vector<int>> gcons_list(groups_.size());
+    for (int t = 0; t < n; ++t) {
+      gleft[task_group_[t]]++;
+      unmet[t] = (int)task_waits_[t].size();
+      for (int g : task_waits_[t]) gcons_list[g].push_back(t);
+    }
+    typedef std::pair<double, int> PI;
+    std::priority_queue<PI> ready;  // (bottom level, -index)
+    std::priority_queue<PI, std::vector<PI>, std::greater<PI>> running;  // (finish, task)
+    for (size_t g = 0; g < groups_.size(); ++g)  // empty groups are complete at once
+      if (gleft[g] == 0)
+        for (int c : gcons_list[g]) --unmet[c];
+    for (int t = 0; t < n; ++t)
+      if (unmet[t] == 0) ready.push(PI(bl[t], -t));
+    std::vector<int> order;
+    order.reserve(n);
+    int busy = 0;
+    double now = 0.0;
+    while ((int)order.size() < n) {
+      while (busy < pp_.ctas && !ready.empty()) {
+        const int t = -ready.top().second;
+        ready.pop();
+        order.push_back(t);
+        running.push(PI(now + dur[t], t));
+        ++busy;
+      }
+      if (running.empty()) {  // cannot happen for a DAG; keep every task regardless
+        for (int t = 0; t < n; ++t)
+          if (std::find(order.begin(), order.end(), t) == order.end()) order.push_back(t);
+        break;
+      }
+      const PI ev = running.top();
+      running.pop();
+      --busy;
+      now = ev.first;
+      const int g = task_group_[ev.second];
+      if (--gleft[g] == 0)
+        for (int c : gcons_list[g])
+          if (--unmet[c] == 0) ready.push(PI(bl[c], -c));
+    }
     Program out;
+    out.overflow = overflow_;
     out.terms = prog_.terms;
     out.eyes = prog_.eyes;
+    out.ents = prog_.ents;
     out.t_elems = prog_.t_elems;
     out.term_bytes = prog_.term_bytes;
     out.algo_bytes = prog_.algo_bytes;
@@ -242,6 +298,7 @@ class Builder {
   std::vector<int> task_group_;
   std::vector<double> task_cost_;
   std::set<int64_t> sweep_kernels_;
+  bool overflow_ = false;
 };
 
 bool same_scale(const TermSpec& t, const HostEntry& e) {

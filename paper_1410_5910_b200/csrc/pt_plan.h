@@ -30,7 +30,7 @@ struct Operator {
   std::vector<DevSlot> slots;
   std::vector<DevKernelPLR> kplr;
   std::vector<int32_t> tile_ptr;
-  std::vector<int32_t> tile_leaves;
+  std::vector<DevTileEntry> tile_ent;
   std::vector<int32_t> nslot;  // per kernel: sum of ranks
 };
 
@@ -39,11 +39,13 @@ struct Program {
   std::vector<DevTerm> terms;
   std::vector<DevEye> eyes;
   std::vector<DevWait> waits;
+  std::vector<DevTileEntry> ents;  // Y_PLR task entries (t0 absolute, pre = prefix)
   int n_counters = 0;
   int64_t t_elems = 0;      // size of SLOT_T needed
   int64_t term_bytes = 0;   // kernel bytes actually streamed by the terms
   int64_t algo_bytes = 0;   // distinct kernels per apply/sweep
   int64_t slot_elems[N_SLOTS] = {0};  // minimum size of each slot vector
+  bool overflow = false;    // a Y_PLR task exceeds MAX_TILE_ENTRIES (not runnable)
   std::string describe() const;
 };
 
@@ -54,6 +56,9 @@ std::string sweep_diagonal_error(const Operator& op);
 
 // Program kinds.
 struct PlanParams {
+  int ctas = 444;                // executor CTAs (queue-order simulation)
+  double task_us = 2.0;          // fixed cost per task in the simulation
+  double cta_gbs = 25.0;         // streaming rate of one CTA in the simulation
   int dense_rows_per_task = 16;  // Y_DENSE rows per task
   int plr_rows_per_task = PLR_TILE;  // Y_PLR rows per task (lane per row)
   int plr_slots_per_task = 64;   // T_PLR slots per task (warp per slot)

@@ -71,6 +71,7 @@ struct DevTask {
   VecRef init;         // Y: partial sum to start from
   VecRef rhs;          // Y: + rhs_coef * rhs
   double rhs_coef;
+  int32_t ent0, nent;  // Y_PLR: flat tile entries of all terms (program ents array)
 };
 
 // PLR storage on the device.  For each leaf the factors are stored as
@@ -88,12 +89,26 @@ struct DevSlot {     // one Vt row, for the t-phase
 };
 
 constexpr int PLR_TILE = 32;  // rows of a Y_PLR task (one per lane)
+constexpr int MAX_TILE_ENTRIES = 256;  // leaf entries of one Y_PLR task (all terms)
 
 struct DevKernelPLR {
   int32_t leaf0, nleaf;      // into the leaf table
   int32_t slot0, nslot;      // into the slot table (nslot = sum of ranks)
-  int32_t tile0;             // leaves meeting row tile t: tile_leaves[tile_ptr[tile0+t] ..
-  int32_t pad;               //                                    tile_ptr[tile0+t+1])
+  int32_t tile0;             // leaves meeting row tile t: tile_ent[tile_ptr[tile0+t] ..
+  int32_t pad;               //                                  tile_ptr[tile0+t+1])
+};
+
+// One leaf as seen from one PLR_TILE-row tile: lanes [lo, hi) of the tile
+// lie inside the leaf; lane l reads U column c at u0 + c*stride + (l - lo).
+struct DevTileEntry {
+  int64_t u0;
+  int32_t t0;      // first slot of the leaf (kernel-relative in the operator table,
+                   // absolute SLOT_T index in a program's task entries)
+  int32_t stride;  // leaf rows (U is column-major)
+  int32_t rank;
+  int32_t pre;     // task entries: columns of the preceding entries of the task
+  int16_t lo, hi;
+  int32_t pad;
 };
 
 }  // namespace pt
