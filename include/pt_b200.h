@@ -114,6 +114,12 @@ int pt_apply_A(pt_handle *h, const double *x, double *y, pt_stream stream);
 int pt_apply_M(pt_handle *h, const double *r, double *z, int32_t n_it,
                pt_stream stream);
 
+/* w = M^-1 (A x): one GMRES iteration's preconditioned matvec
+ * (solver.py:254) as ONE fused launch -- the sweeps start on A's output
+ * blocks as they are produced. */
+int pt_apply_AM(pt_handle *h, const double *x, double *w, int32_t n_it,
+                pt_stream stream);
+
 /* u_out = D^-1 (P rhs - R u_in)   (gs_sweep, solver.py:203-220). */
 int pt_gs_sweep(pt_handle *h, const double *rhs, const double *u_in,
                 double *u_out, pt_stream stream);
@@ -177,6 +183,11 @@ int pt_exec_stats(pt_handle *h, double *total_ms, int64_t *launches,
  * for every task q in queue order.  Profiling aid; synchronises. */
 int pt_trace_program(pt_handle *h, int32_t kind, int32_t n_it, const double *in,
                      double *out, int64_t *rec, int64_t cap, int64_t *n_out);
+
+/* Executor launch shape: CTAs (cooperative grid), dynamic smem per CTA and
+ * the complex capacity of one operator staging buffer half. */
+int pt_exec_info(const pt_handle *h, int32_t *grid, int64_t *smem_bytes,
+                 int64_t *half_elems);
 
 /* ---- misc ----------------------------------------------------------------*/
 const char *pt_last_error(void);

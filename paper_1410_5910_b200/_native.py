@@ -56,6 +56,7 @@ _SIGS = {
     "pt_apply_A": (C.c_int, [_VP, _VP, _VP, _VP]),
     "pt_apply_M": (C.c_int, [_VP, _VP, _VP, C.c_int32, _VP]),
     "pt_gs_sweep": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "pt_apply_AM": (C.c_int, [_VP, _VP, _VP, C.c_int32, _VP]),
     "pt_gmres": (C.c_int, [_VP, _VP, _VP, C.POINTER(GmresConfigC), C.POINTER(Report), _VP]),
     "pt_gmres_host": (C.c_int, [_VP, _VP, _VP, C.POINTER(GmresConfigC), C.POINTER(Report), _VP]),
     "pt_gmres_batch": (C.c_int, [_VP, _VP, _VP, C.c_int32, C.POINTER(GmresConfigC),
@@ -72,6 +73,8 @@ _SIGS = {
                                 C.POINTER(C.c_int64)]),
     "pt_trace_program": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP, C.POINTER(C.c_int64),
                                    C.c_int64, C.POINTER(C.c_int64)]),
+    "pt_exec_info": (C.c_int, [_VP, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                               C.POINTER(C.c_int64)]),
     "pt_last_error": (C.c_char_p, []),
     "pt_abi_version": (C.c_int32, []),
     "pt_launch_count": (C.c_int64, []),

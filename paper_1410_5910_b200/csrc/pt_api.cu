@@ -55,8 +55,10 @@ struct DevProgram {
   DevEye* eyes = nullptr;
   DevWait* waits = nullptr;
   DevTileEntry* ents = nullptr;
+  DevPiece* pieces = nullptr;
   ~DevProgram() {
     cudaFree(ents);
+    cudaFree(pieces);
     cudaFree(tasks);
     cudaFree(terms);
     cudaFree(eyes);
@@ -123,6 +125,7 @@ struct pt_handle {
   int ctr_cap = 0;
   int grid = 0;
   size_t smem = 0;
+  int64_t src_cap = 0;
   std::unique_ptr<pt_gmres_ws> gws;
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
@@ -179,6 +182,13 @@ struct pt_handle {
 
 namespace {
 
+// Device layout of the PLR factors, per kernel:
+//   Vt region  -- every slot's Vt row (leaf order, rank order), contiguous,
+//                 so the slots of a T task are one bulk copy;
+//   U chunks   -- per PLR_TILE-row tile: for each leaf meeting the tile, for
+//                 each rank column, the tile's rows of U*Sigma (column-major
+//                 pieces), so the U data of one Y task term is one range.
+// Bytes are the reference's factor bytes (plus 128-byte alignment pads).
 int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, const double* fac,
                      int64_t n_fac) {
   Operator& op = h->op;
@@ -202,83 +212,87 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
   auto align8 = [&]() {
     while (blob.size() % 8) blob.push_back(make_double2(0.0, 0.0));
   };
+  auto U = [&](const pt_leaf& L, int64_t r, int64_t c) {  // (U*Sigma)[r, c], row-major input
+    const double* z = fac + 2 * (L.u_off + r * L.rank + c);
+    return make_double2(z[0], z[1]);
+  };
   op.kplr.assign(op.nk, DevKernelPLR{});
   op.nslot.assign(op.nk, 0);
   op.kernel_bytes.assign(op.nk, 0);
+  const int64_t ntiles = (m + PLR_TILE - 1) / PLR_TILE;
   size_t pos = 0;
   for (int k = 0; k < op.nk; ++k) {
     DevKernelPLR& kp = op.kplr[k];
     kp.leaf0 = (int32_t)op.leaves.size();
     kp.slot0 = (int32_t)op.slots.size();
-    int32_t slot = 0;
+    std::vector<const pt_leaf*> kl;
     for (; pos < idx.size() && leaves[idx[pos]].kernel == k; ++pos) {
       const pt_leaf& L = leaves[idx[pos]];
       op.kernel_bytes[k] += 16 * L.rank * (L.rows + L.cols);
-      if (L.rank == 0) continue;
+      if (L.rank > 0) kl.push_back(&L);
+    }
+    // Vt region
+    align8();
+    int32_t slot = 0;
+    for (const pt_leaf* L : kl) {
       DevLeaf dl{};
-      align8();
-      dl.u_off = (int64_t)blob.size();
-      const double* U = fac + 2 * L.u_off;
-      for (int64_t c = 0; c < L.rank; ++c)
-        for (int64_t r = 0; r < L.rows; ++r) {
-          const double* z = U + 2 * (r * L.rank + c);
-          blob.push_back(make_double2(z[0], z[1]));
-        }
-      align8();
-      dl.v_off = (int64_t)blob.size();
-      const double* Vt = fac + 2 * L.vt_off;
-      for (int64_t i = 0; i < L.rank * L.cols; ++i) blob.push_back(make_double2(Vt[2 * i], Vt[2 * i + 1]));
-      dl.row_off = (int32_t)L.row_off;
-      dl.col_off = (int32_t)L.col_off;
-      dl.rows = (int32_t)L.rows;
-      dl.cols = (int32_t)L.cols;
-      dl.rank = (int32_t)L.rank;
+      dl.row_off = (int32_t)L->row_off;
+      dl.col_off = (int32_t)L->col_off;
+      dl.rows = (int32_t)L->rows;
+      dl.cols = (int32_t)L->cols;
+      dl.rank = (int32_t)L->rank;
       dl.slot0 = slot;
-      for (int64_t c = 0; c < L.rank; ++c) {
-        DevSlot s{};
-        s.v_off = dl.v_off + c * L.cols;
-        s.col_off = dl.col_off;
-        s.cols = dl.cols;
-        op.slots.push_back(s);
+      dl.v_off = (int64_t)blob.size();
+      const double* Vt = fac + 2 * L->vt_off;
+      for (int64_t c = 0; c < L->rank; ++c) {
+        DevSlot sl{};
+        sl.v_off = (int64_t)blob.size();
+        sl.col_off = dl.col_off;
+        sl.cols = dl.cols;
+        op.slots.push_back(sl);
+        for (int64_t j = 0; j < L->cols; ++j)
+          blob.push_back(make_double2(Vt[2 * (c * L->cols + j)], Vt[2 * (c * L->cols + j) + 1]));
       }
-      slot += (int32_t)L.rank;
+      slot += (int32_t)L->rank;
       op.leaves.push_back(dl);
     }
     kp.nleaf = (int32_t)op.leaves.size() - kp.leaf0;
     kp.nslot = slot;
     op.nslot[k] = slot;
-    // leaves meeting each PLR_TILE-row tile, in leaf (slot) order
-    const int64_t ntiles = (m + PLR_TILE - 1) / PLR_TILE;
+    // tile-major U chunks
     kp.tile0 = (int32_t)op.tile_ptr.size();
     for (int64_t t = 0; t < ntiles; ++t) {
+      align8();
       op.tile_ptr.push_back((int32_t)op.tile_ent.size());
+      op.tile_chunk.push_back((int64_t)blob.size());
       const int64_t lo = t * PLR_TILE, hi = std::min<int64_t>(m, lo + PLR_TILE);
-      for (int32_t l = kp.leaf0; l < kp.leaf0 + kp.nleaf; ++l) {
-        const DevLeaf& dl = op.leaves[l];
+      for (int32_t l = 0; l < kp.nleaf; ++l) {
+        const DevLeaf& dl = op.leaves[kp.leaf0 + l];
         if (!(dl.row_off < hi && dl.row_off + dl.rows > lo)) continue;
-        DevTileEntry te{};
+        const pt_leaf& L = *kl[l];
         const int64_t r_first = std::max<int64_t>(lo, dl.row_off);
         const int64_t r_end = std::min<int64_t>(hi, dl.row_off + dl.rows);
-        te.u0 = dl.u_off + (r_first - dl.row_off);
+        DevTileEntry te{};
+        te.u0 = (int64_t)blob.size();
         te.t0 = dl.slot0;
-        te.stride = dl.rows;
+        te.stride = (int32_t)(r_end - r_first);
         te.rank = dl.rank;
         te.lo = (int16_t)(r_first - lo);
         te.hi = (int16_t)(r_end - lo);
+        for (int64_t c = 0; c < L.rank; ++c)
+          for (int64_t r = r_first; r < r_end; ++r) blob.push_back(U(L, r - dl.row_off, c));
         op.tile_ent.push_back(te);
       }
     }
     op.tile_ptr.push_back((int32_t)op.tile_ent.size());
+    op.tile_chunk.push_back((int64_t)blob.size());
   }
   if (op.tile_ent.empty()) op.tile_ent.push_back(DevTileEntry{});
   if (blob.empty()) blob.push_back(make_double2(0.0, 0.0));
   int rc;
   if ((rc = upload(&h->fac, blob))) return rc;
-  if ((rc = upload(&h->leaves, op.leaves))) return rc;
   if ((rc = upload(&h->slots, op.slots))) return rc;
   if ((rc = upload(&h->kplr, op.kplr))) return rc;
-  if ((rc = upload(&h->tile_ptr, op.tile_ptr))) return rc;
-  if ((rc = upload(&h->tile_ent, op.tile_ent))) return rc;
   return 0;
 }
 
@@ -319,6 +333,7 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
   if ((rc = upload(&p->eyes, p->host.eyes))) return rc;
   if ((rc = upload(&p->waits, p->host.waits))) return rc;
   if ((rc = upload(&p->ents, p->host.ents))) return rc;
+  if ((rc = upload(&p->pieces, p->host.pieces))) return rc;
   for (int s : {SLOT_Y, SLOT_U1, SLOT_U2, SLOT_PRE, SLOT_T})
     if ((rc = ensure_slot(h, s, p->host.slot_elems[s]))) return rc;
   if (p->host.n_counters + 1 > h->ctr_cap) {
@@ -361,6 +376,9 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.tile_ptr = h->tile_ptr;
   a.tile_ent = h->tile_ent;
   a.ents = p->ents;
+  a.pieces = p->pieces;
+  a.half_elems = h->pp.half_elems;
+  a.src_cap = h->src_cap;
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
   a.stop = stop;
@@ -556,24 +574,55 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     if (n_leaves > 0 && (!leaves || !factors)) return fail(PT_EINVAL, "PLR tables missing");
     if ((rc = build_plr_tables(h.get(), leaves, n_leaves, factors, n_factor_complex))) return rc;
   }
-  // [source staging: m][partials: EXEC_THREADS][task metadata: MAX_TILE_ENTRIES entries]
-  h->smem = ((size_t)op.m + EXEC_THREADS) * sizeof(double2) +
-            MAX_TILE_ENTRIES * sizeof(DevTileEntry);
-  if (h->smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)h->smem));
+  // Shared memory per CTA: [two operator buffer halves][source / t staging]
+  // [partials][task metadata].  The halves take what is left after the fixed
+  // part at the largest CTA count per SM (<= 3, or PT_CTAS_PER_SM) for which
+  // one half still holds the largest contiguous unit a task stages (a dense
+  // row, a Vt row).
+  h->src_cap = std::max<int64_t>(op.m, MAX_TCOLS);
+  const size_t meta = std::max(MAX_TILE_ENTRIES * sizeof(DevTileEntry), MAX_T_SLOTS * sizeof(DevSlot));
+  const size_t fixed = ((size_t)h->src_cap + EXEC_THREADS) * sizeof(double2) + meta;
+  int64_t need = op.m;  // dense: one kernel row
+  if (op.fmt == PT_KERNEL_PLR) {
+    need = PLR_TILE;
+    for (const DevSlot& sl : op.slots) need = std::max<int64_t>(need, sl.cols);
+  }
+  int smem_sm = 0, smem_blk = 0;
+  CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+  CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  int target = 3;
+  if (const char* e = std::getenv("PT_CTAS_PER_SM")) target = std::max(1, std::min(4, std::atoi(e)));
+  cudaFuncAttributes fa{};
+  CK(cudaFuncGetAttributes(&fa, pt_exec_kernel));
+  int reserved = 1024;
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+  int64_t half = 0;
+  for (int c = target; c >= 1; --c) {
+    const int64_t per_cta =
+        std::min<int64_t>(smem_sm / c - reserved - (int64_t)fa.sharedSizeBytes - 128, smem_blk);
+    const int64_t hb = (per_cta - (int64_t)fixed) / 2;
+    half = hb > 0 ? (hb / (int64_t)sizeof(double2)) / 8 * 8 : 0;
+    if (half >= need) break;
+  }
+  if (half < need) return fail(PT_EINVAL, "block size too large for the executor's shared memory");
+  h->pp.half_elems = half;
+  h->smem = 2 * (size_t)half * sizeof(double2) + fixed;
+  CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)h->smem));
   int nsm = 0, occ = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_exec_kernel, EXEC_THREADS, h->smem));
   if (occ < 1) return fail(PT_EINVAL, "executor kernel does not fit on an SM");
   h->grid = nsm * occ;
   h->pp.ctas = h->grid;
-  h->pp.dense_rows_per_task = DENSE_ROWS_PER_TASK;
+  h->pp.dense_rows_per_task =
+      (int)std::max<int64_t>(1, std::min<int64_t>(DENSE_RT_MAX, half / std::max<int64_t>(op.m, 1)));
   h->pp.plr_rows_per_task = PLR_TILE;
-  h->pp.plr_slots_per_task = 16;
+  h->pp.plr_slots_per_task = MAX_T_SLOTS;
   if (const char* e = std::getenv("PT_DENSE_ROWS"))
     h->pp.dense_rows_per_task = std::max(1, std::min(DENSE_RT_MAX, std::atoi(e)));
   if (const char* e = std::getenv("PT_T_SLOTS")) h->pp.plr_slots_per_task = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PT_T_PIECES")) h->pp.t_pieces = std::max(1, std::atoi(e));
   CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
   *out = h.release();
   return 0;
@@ -608,6 +657,20 @@ int pt_apply_M(pt_handle* h, const double* r, double* z, int32_t n_it, pt_stream
   int rc = get_program(h, "M", n_it, &p);
   if (rc) return rc;
   if ((rc = run_program(h, p, (const double2*)r, (double2*)z, nullptr, (cudaStream_t)stream)))
+    return rc;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int pt_apply_AM(pt_handle* h, const double* x, double* w, int32_t n_it, pt_stream stream) {
+  if (!h || !x || !w) return fail(PT_EINVAL, "null argument");
+  if (n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
+  if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  DeviceGuard guard(h->device);
+  DevProgram* p;
+  int rc = get_program(h, "AM", n_it, &p);
+  if (rc) return rc;
+  if ((rc = run_program(h, p, (const double2*)x, (double2*)w, nullptr, (cudaStream_t)stream)))
     return rc;
   CK(cudaGetLastError());
   return 0;
@@ -1000,6 +1063,14 @@ int pt_trace_program(pt_handle* h, int32_t kind, int32_t n_it, const double* in,
     r[10] = t.type == TASK_T_PLR ? p->host.terms[t.term0].kernel : -1;
     r[11] = t.signal;
   }
+  return 0;
+}
+
+int pt_exec_info(const pt_handle* h, int32_t* grid, int64_t* smem_bytes, int64_t* half_elems) {
+  if (!h) return fail(PT_EINVAL, "null handle");
+  if (grid) *grid = h->grid;
+  if (smem_bytes) *smem_bytes = (int64_t)h->smem;
+  if (half_elems) *half_elems = h->pp.half_elems;
   return 0;
 }
 

@@ -82,6 +82,9 @@ struct ExecArgs {
   const int32_t* tile_ptr;
   const DevTileEntry* tile_ent;
   const DevTileEntry* ents;  // program's Y_PLR task entries
+  const DevPiece* pieces;    // program's staged operator ranges
+  int64_t half_elems;        // complex capacity of one smem buffer half
+  int64_t src_cap;           // complex capacity of the source / t staging area
   const int* stop;  // GMRES status stop flag: the whole launch is skipped once set
   // iteration-relative basis addressing (GMRES loop inside a graph):
   // if iter != nullptr, SLOT_IN = vbase + (*iter) * vstride, SLOT_OUT = SLOT_IN + vstride

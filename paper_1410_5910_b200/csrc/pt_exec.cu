@@ -9,44 +9,96 @@
 // counter always has a running producer: no deadlock, no grid barrier, and
 // the sequential sweep chain overlaps the independent A-apply / R-term work.
 //
-// A task runs in three phases:
-//   prepare  -- before its inputs are ready: issue TMA bulk prefetches
-//               (cp.async.bulk.prefetch.L2) of the kernel data it will
-//               stream and stage its metadata in smem.  Kernel data never
-//               depends on the iterate, so HBM streaming of a sweep level
-//               overlaps the previous level's dependency chain.
-//   wait     -- thread 0 acquires the producer counters.
-//   compute  -- 16-byte complex loads (now mostly L2 hits), FP64 FMA,
-//               fixed-order reductions.
-//
-// Kernel data is read with ld.global.nc.L1::no_allocate; vectors written
-// during the launch are read through L2 (ld.cg).  Each output element is
-// produced by one CTA in a fixed order, so repeated applies are bitwise
-// identical (no float atomics).
+// Operator data moves HBM -> shared memory with TMA bulk copies
+// (cp.async.bulk.shared::cluster.global, completion on an mbarrier).  Every
+// task's operator bytes are a few contiguous "pieces" (host layout: a Vt
+// region per kernel and tile-major U chunks), double-buffered in two smem
+// halves.  The first two pieces are issued when the task is grabbed, BEFORE
+// its dependency wait: the operator never depends on the iterate, so a sweep
+// level's kernels stream in while the previous level is still computing.
+// After the wait the task stages its (small) vector inputs, waits for the
+// pieces and computes from shared memory (FP64 FMA, fixed-order sums, no
+// float atomics: repeated applies are bitwise identical).
 #include "pt_device.cuh"
 
 namespace pt {
 
 namespace {
 
-// slot base pointers of this launch (iteration-relative ones resolved), in smem
+// slot base pointers of this launch (iteration-relative ones resolved)
 __shared__ double2* s_slot[N_SLOTS];
+__shared__ __align__(8) unsigned long long s_bar[2];  // one mbarrier per buffer half
 
 __device__ __forceinline__ const double2* vptr(const VecRef& r) { return s_slot[r.slot] + r.off; }
 __device__ __forceinline__ double2* vptr_w(const VecRef& r) { return s_slot[r.slot] + r.off; }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// thread 0: stage one piece into a buffer half (TMA bulk copy, mbarrier tx)
+__device__ __forceinline__ void issue_piece(unsigned long long* bar, double2* dst,
+                                            const double2* src, uint32_t bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void wait_bar(unsigned long long* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
 struct Smem {
-  double2* src;        // m: staged source vector
-  double2* part;       // EXEC_THREADS: partial sums
-  DevTileEntry* ent;   // MAX_TILE_ENTRIES: task metadata (Y_PLR entries / T slots)
+  double2* half[2];    // operator piece buffers
+  double2* src;        // staged source vector (m) / t values (MAX_TCOLS)
+  double2* part;       // EXEC_THREADS partial sums
+  void* meta;          // task metadata (entries / slots)
 };
 
-__device__ __forceinline__ Smem carve(double2* base, int m) {
+__device__ __forceinline__ Smem carve(double2* base, const ExecArgs& a) {
   Smem s;
-  s.src = base;
-  s.part = base + m;
-  s.ent = reinterpret_cast<DevTileEntry*>(base + m + EXEC_THREADS);
+  s.half[0] = base;
+  s.half[1] = base + a.half_elems;
+  s.src = base + 2 * a.half_elems;
+  s.part = s.src + a.src_cap;
+  s.meta = s.part + EXEC_THREADS;
   return s;
+}
+
+// per-CTA pipeline state (uniform across threads)
+struct Pipe {
+  uint32_t phase[2];
+};
+
+__device__ __forceinline__ const double2* pool_of(const ExecArgs& a, const DevTask& t) {
+  return t.type == TASK_Y_DENSE ? a.dense : a.fac;
+}
+
+// thread 0 issues piece p of task t into half p % 2
+__device__ __forceinline__ void issue(const ExecArgs& a, const DevTask& t, const Smem& sm, int p) {
+  const DevPiece pc = a.pieces[t.piece0 + p];
+  issue_piece(&s_bar[p & 1], sm.half[p & 1], pool_of(a, t) + pc.src,
+              (uint32_t)pc.elems * (uint32_t)sizeof(double2));
+}
+
+__device__ __forceinline__ const double2* wait_piece(Pipe& pp, int p, const Smem& sm) {
+  wait_bar(&s_bar[p & 1], pp.phase[p & 1]);
+  pp.phase[p & 1] ^= 1u;
+  return sm.half[p & 1];
 }
 
 // stage x_a [+ x_b] (length m) into smem
@@ -76,43 +128,44 @@ __device__ __forceinline__ void finish_row(const ExecArgs& a, const DevTask& t, 
   st_cg(vptr_w(t.out) + row, v);
 }
 
-// ---- Y_DENSE ------------------------------------------------------------------
+// ---- metadata staging (before the dependency wait) --------------------------------
 
-__device__ void prepare_y_dense(const ExecArgs& a, const DevTask& t) {
-  if ((int)threadIdx.x < t.nterm) {
-    const DevTerm tm = a.terms[t.term0 + threadIdx.x];
-    const int m = a.m;
-    prefetch_l2(a.dense + ((size_t)tm.kernel * m + t.r0) * m,
-                (uint32_t)((t.r1 - t.r0) * (size_t)m * sizeof(double2)));
+__device__ __forceinline__ void stage_meta(const ExecArgs& a, const DevTask& t, const Smem& sm) {
+  if (t.type == TASK_Y_PLR) {
+    DevTileEntry* ent = reinterpret_cast<DevTileEntry*>(sm.meta);
+    for (int i = threadIdx.x; i < t.nent; i += EXEC_THREADS) ent[i] = a.ents[t.ent0 + i];
+  } else if (t.type == TASK_T_PLR) {
+    const DevTerm tm = a.terms[t.term0];
+    const int32_t slot0 = a.kplr[tm.kernel].slot0;
+    DevSlot* sl = reinterpret_cast<DevSlot*>(sm.meta);
+    for (int q = threadIdx.x; q < t.r1 - t.r0; q += EXEC_THREADS) sl[q] = a.slots[slot0 + t.r0 + q];
   }
 }
 
-// Up to DENSE_RT_MAX rows from dense kernel terms.  Columns are split over
-// the 8 warps (warp w takes columns 32w + lane + 256 i); each warp keeps its
-// scaled partial per row in smem and the partials are added in warp order.
-__device__ void run_y_dense(const ExecArgs& a, const DevTask& t, const Smem& sm) {
+// ---- Y_DENSE: rows [r0, r1) from dense kernel terms -------------------------------
+// piece p = rows r0..r1 of term p's kernel (row-major, staged in smem).
+// Columns are split over the 8 warps; each warp keeps its scaled partial per
+// row in smem; partials are added in warp order.
+__device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t, const Smem& sm, Pipe& pp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.m;
   const int nrows = t.r1 - t.r0;
   double2* part = sm.part;  // [EXEC_WARPS][DENSE_RT_MAX]
   if (lane < DENSE_RT_MAX) part[warp * DENSE_RT_MAX + lane] = make_double2(0.0, 0.0);
+  __syncthreads();  // partials visible to the final sum even when there are no terms
   for (int it = 0; it < t.nterm; ++it) {
     const DevTerm tm = a.terms[t.term0 + it];
-    __syncthreads();
     stage_source(tm, sm.src, m);
     __syncthreads();
-    const double2* K = a.dense + ((size_t)tm.kernel * m + t.r0) * m;
+    const double2* K = wait_piece(pp, it, sm);
     double2 d[DENSE_RT_MAX];
 #pragma unroll
     for (int k = 0; k < DENSE_RT_MAX; ++k) d[k] = make_double2(0.0, 0.0);
     for (int c = 32 * warp + lane; c < m; c += EXEC_THREADS) {
-      double2 kv[DENSE_RT_MAX];
-#pragma unroll
-      for (int k = 0; k < DENSE_RT_MAX; ++k)
-        kv[k] = k < nrows ? ld_stream(K + (size_t)k * m + c) : make_double2(0.0, 0.0);
       const double2 sv = sm.src[c];
 #pragma unroll
-      for (int k = 0; k < DENSE_RT_MAX; ++k) d[k] = cfma(kv[k], sv, d[k]);
+      for (int k = 0; k < DENSE_RT_MAX; ++k)
+        if (k < nrows) d[k] = cfma(K[k * m + c], sv, d[k]);
     }
     const double2 sc = make_double2(tm.scale_re, tm.scale_im);
 #pragma unroll
@@ -121,142 +174,115 @@ __device__ void run_y_dense(const ExecArgs& a, const DevTask& t, const Smem& sm)
       if (lane == k && k < nrows)
         part[warp * DENSE_RT_MAX + k] = cfma(sc, r, part[warp * DENSE_RT_MAX + k]);
     }
+    __syncthreads();  // buffer half and source free
+    if (threadIdx.x == 0 && it + 2 < t.npiece) issue(a, t, sm, it + 2);
   }
-  __syncthreads();
   if ((int)threadIdx.x >= nrows) return;
   double2 v = make_double2(0.0, 0.0);
   for (int w = 0; w < EXEC_WARPS; ++w) v = cadd(v, part[w * DENSE_RT_MAX + threadIdx.x]);
   finish_row(a, t, t.r0 + threadIdx.x, v);
 }
 
-// ---- T_PLR ----------------------------------------------------------------------
-
-__device__ void prepare_t_plr(const ExecArgs& a, const DevTask& t, const Smem& sm) {
-  const DevTerm tm = a.terms[t.term0];
-  const int32_t slot0 = a.kplr[tm.kernel].slot0;
-  DevSlot* sl = reinterpret_cast<DevSlot*>(sm.ent);
-  for (int q = threadIdx.x; q < t.r1 - t.r0; q += EXEC_THREADS) {
-    const DevSlot d = a.slots[slot0 + t.r0 + q];
-    sl[q] = d;
-    prefetch_l2(a.fac + d.v_off, (uint32_t)d.cols * sizeof(double2));
-  }
-}
-
-// t = scale * Vt (x_a [+ x_b]) for a slot range of one PLR term: source staged
-// in smem, warp per Vt row (two rows in flight per warp), lanes across
-// columns.  The term's scale is folded into t so Y is a plain U t sum.
-__device__ void run_t_plr(const ExecArgs& a, const DevTask& t, const Smem& sm) {
+// ---- T_PLR: t = scale * Vt (x_a [+ x_b]) for a slot range ----------------------------
+// The Vt rows of the task are one piece (contiguous in the Vt region); warp per
+// Vt row, lanes across columns, everything from smem.  The term's scale is
+// folded into t so the Y phase is a plain U t sum.
+__device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, const Smem& sm, Pipe& pp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m = a.m;
   const DevTerm tm = a.terms[t.term0];
   double2* T = s_slot[SLOT_T] + tm.t_base;
-  stage_source(tm, sm.src, m);
+  stage_source(tm, sm.src, a.m);
   __syncthreads();
-  const DevSlot* sl = reinterpret_cast<const DevSlot*>(sm.ent);
+  const DevSlot* sl = reinterpret_cast<const DevSlot*>(sm.meta);
   const double2 sc = make_double2(tm.scale_re, tm.scale_im);
-  const int ns = t.r1 - t.r0;
-  for (int q = warp; q < ns; q += 2 * EXEC_WARPS) {
-    const int q2 = q + EXEC_WARPS;
-    const DevSlot d1 = sl[q];
-    const bool has2 = q2 < ns;
-    const DevSlot d2 = has2 ? sl[q2] : d1;
-    const int n2 = has2 ? d2.cols : 0;
-    const double2* V1 = a.fac + d1.v_off;
-    const double2* V2 = a.fac + d2.v_off;
-    const double2* x1 = sm.src + d1.col_off;
-    const double2* x2 = sm.src + d2.col_off;
-    double2 r1 = make_double2(0.0, 0.0), r2 = make_double2(0.0, 0.0);
-    const int cmax = max(d1.cols, n2);
-    constexpr int U = 4;
-    for (int c0 = lane; c0 < cmax; c0 += 32 * U) {
-      double2 v1[U], v2[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + 32 * u;
-        v1[u] = c < d1.cols ? ld_stream(V1 + c) : make_double2(0.0, 0.0);
-        v2[u] = c < n2 ? ld_stream(V2 + c) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + 32 * u;
-        if (c < d1.cols) r1 = cfma(v1[u], x1[c], r1);
-        if (c < n2) r2 = cfma(v2[u], x2[c], r2);
-      }
+  for (int p = 0; p < t.npiece; ++p) {
+    const DevPiece pc = a.pieces[t.piece0 + p];
+    const double2* buf = wait_piece(pp, p, sm);
+    for (int q = pc.f0 + warp; q < pc.f1; q += EXEC_WARPS) {
+      const DevSlot d = sl[q];
+      const double2* V = buf + (d.v_off - pc.src);
+      const double2* x = sm.src + d.col_off;
+      double2 r = make_double2(0.0, 0.0);
+      for (int c = lane; c < d.cols; c += 32) r = cfma(V[c], x[c], r);
+      r = warp_sum(r);
+      if (lane == 0) st_cg(T + t.r0 + q, cmul(sc, r));
     }
-    r1 = warp_sum(r1);
-    r2 = warp_sum(r2);
-    if (lane == 0) {
-      st_cg(T + t.r0 + q, cmul(sc, r1));
-      if (has2) st_cg(T + t.r0 + q2, cmul(sc, r2));
-    }
+    __syncthreads();
+    if (threadIdx.x == 0 && p + 2 < t.npiece) issue(a, t, sm, p + 2);
   }
 }
 
-// ---- Y_PLR ----------------------------------------------------------------------
-
-// Stage the task's flat tile entries (host-built: t0 absolute, prefix
-// column counts) in smem and prefetch their U column segments into L2.
-__device__ void prepare_y_plr(const ExecArgs& a, const DevTask& t, const Smem& sm) {
-  for (int i = threadIdx.x; i < t.nent; i += EXEC_THREADS) {
-    const DevTileEntry e = a.ents[t.ent0 + i];
-    sm.ent[i] = e;
-    const uint32_t bytes = (uint32_t)(e.hi - e.lo) * sizeof(double2);
-    for (int c = 0; c < e.rank; ++c) prefetch_l2(a.fac + e.u0 + (int64_t)c * e.stride, bytes);
-  }
-}
-
-// One PLR_TILE-row tile of an output block: y_r = sum over the staged
-// entries of U_leaf[r, :] t_leaf.  Lane = row (U is column-major: a warp
-// reads up to 32 consecutive rows of one rank column, contiguous bytes); the
-// (entry, column) pairs are dealt round-robin to the 8 warps, and the 8
-// partial sums per row are added in warp order.
-__device__ void run_y_plr(const ExecArgs& a, const DevTask& t, const Smem& sm) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = t.r0 + lane;
-  const double2* T = s_slot[SLOT_T];
-  const int count = t.nent;
-  const int ncol = count ? sm.ent[count - 1].pre + sm.ent[count - 1].rank : 0;
-  double2 acc = make_double2(0.0, 0.0);
-  constexpr int B = 8;  // independent columns in flight per warp
-  int e = 0;
-  for (int f0 = warp; f0 < ncol; f0 += B * EXEC_WARPS) {
-    double2 uv[B], tv[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const int f = f0 + b * EXEC_WARPS;
-      uv[b] = make_double2(0.0, 0.0);
-      tv[b] = make_double2(0.0, 0.0);
-      if (f < ncol) {
-        while (e + 1 < count && f >= sm.ent[e + 1].pre) ++e;
-        const DevTileEntry en = sm.ent[e];
-        const int c = f - en.pre;
-        if (lane >= en.lo && lane < en.hi)
-          uv[b] = ld_stream(a.fac + en.u0 + (int64_t)c * en.stride + (lane - en.lo));
-        tv[b] = ld_cg(T + en.t0 + c);
-      }
+// ---- Y_PLR: one PLR_TILE-row tile ---------------------------------------------------
+// y_r = sum over the task's flat (entry, rank column) list of U[r, c] t[c].
+// Thread = (row r = tid % 16, column group g = tid / 16): group g takes flat
+// columns f = g (mod 16) in ascending order; the 16 partial sums per row are
+// added in group order.  U pieces and the t values are read from smem.
+__device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, const Smem& sm, Pipe& pp) {
+  constexpr int G = EXEC_THREADS / PLR_TILE;  // 16 column groups
+  const int r = threadIdx.x % PLR_TILE, g = threadIdx.x / PLR_TILE;
+  const DevTileEntry* ent = reinterpret_cast<const DevTileEntry*>(sm.meta);
+  // t values of every flat column (produced by this level's T tasks)
+  double2* ts = sm.src;
+  {
+    const double2* T = s_slot[SLOT_T];
+    int e = 0;
+    for (int f = threadIdx.x; f < t.ncol; f += EXEC_THREADS) {
+      while (e + 1 < t.nent && f >= ent[e + 1].pre) ++e;
+      ts[f] = ld_cg(T + ent[e].t0 + (f - ent[e].pre));
     }
-#pragma unroll
-    for (int b = 0; b < B; ++b) acc = cfma(uv[b], tv[b], acc);
   }
-  sm.part[warp * 32 + lane] = acc;
   __syncthreads();
-  if (warp != 0 || row >= t.r1) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int p = 0; p < t.npiece; ++p) {
+    const DevPiece pc = a.pieces[t.piece0 + p];
+    const double2* buf = wait_piece(pp, p, sm);
+    int e = pc.e0;
+    // first column of this group inside the piece
+    int f = pc.f0 + ((g - pc.f0) % G + G) % G;
+    for (; f < pc.f1; f += G) {
+      while (e + 1 < t.nent && f >= ent[e + 1].pre) ++e;
+      const DevTileEntry en = ent[e];
+      if (r >= en.lo && r < en.hi) {
+        const int c = f - en.pre;
+        const double2 u = buf[en.u0 + (int64_t)c * en.stride - pc.src + (r - en.lo)];
+        acc = cfma(u, ts[f], acc);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && p + 2 < t.npiece) issue(a, t, sm, p + 2);
+  }
+  sm.part[g * PLR_TILE + r] = acc;
+  __syncthreads();
+  if ((int)threadIdx.x >= PLR_TILE || t.r0 + (int)threadIdx.x >= t.r1) return;
   double2 v = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int w = 0; w < EXEC_WARPS; ++w) v = cadd(v, sm.part[w * 32 + lane]);
-  finish_row(a, t, row, v);
+  for (int q = 0; q < G; ++q) v = cadd(v, sm.part[q * PLR_TILE + threadIdx.x]);
+  finish_row(a, t, t.r0 + threadIdx.x, v);
 }
 
 }  // namespace
 
+// thread 0: asynchronous copy of a task descriptor into smem (cp.async)
+__device__ __forceinline__ void fetch_task(DevTask* dst, const DevTask* src) {
+  static_assert(sizeof(DevTask) % 16 == 0, "DevTask must be a multiple of 16 bytes");
+  const char* s = reinterpret_cast<const char*>(src);
+  const uint32_t d = smem_u32(dst);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(DevTask) / 16); ++i)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * i), "l"(s + 16 * i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(EXEC_THREADS, 3) pt_exec_kernel(ExecArgs a) {
-  extern __shared__ double2 smem[];
-  __shared__ int s_task;
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ __align__(16) DevTask s_desc[2];  // current / next task descriptors
+  __shared__ int s_q[2];
+  __shared__ int s_stop;
   if (a.stop) {
-    if (threadIdx.x == 0) s_task = *((volatile const int*)a.stop);
+    if (threadIdx.x == 0) s_stop = *((volatile const int*)a.stop);
     __syncthreads();
-    if (s_task) return;
-    __syncthreads();
+    if (s_stop) return;
   }
   if (threadIdx.x < N_SLOTS) {
     double2* p = a.slot[threadIdx.x];
@@ -266,38 +292,52 @@ __global__ void __launch_bounds__(EXEC_THREADS, 3) pt_exec_kernel(ExecArgs a) {
     }
     s_slot[threadIdx.x] = p;
   }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[i])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int q0 = atomicAdd(a.head, 1);
+    s_q[0] = q0;
+    if (q0 < a.n_tasks) fetch_task(&s_desc[0], a.tasks + q0);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
   __syncthreads();
-  const Smem sm = carve(smem, a.m);
+  const Smem sm = carve(smem, a);
+  Pipe pp;
+  pp.phase[0] = pp.phase[1] = 0;
+  int b = 0;
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(a.head, 1);
-    __syncthreads();
-    const int q = s_task;
-    if (q >= a.n_tasks) return;
-    const DevTask t = a.tasks[q];
+    const int q = s_q[b];
+    if (q >= a.n_tasks) break;
+    const DevTask& t = s_desc[b];
+    int q_next = 0;
     unsigned long long t_grab = 0, t_ready = 0;
-    if (a.trace && threadIdx.x == 0) t_grab = globaltimer();
-    // prepare: prefetch kernel data + stage metadata (independent of the inputs)
-    if (t.type == TASK_Y_DENSE)
-      prepare_y_dense(a, t);
-    else if (t.type == TASK_T_PLR)
-      prepare_t_plr(a, t, sm);
-    else
-      prepare_y_plr(a, t, sm);
-    // wait for the producers of the inputs
+    // grab the next task now; its index is needed only after the wait below
+    if (threadIdx.x == 0) {
+      q_next = atomicAdd(a.head, 1);
+      if (a.trace) t_grab = globaltimer();
+      // prepare: start the operator copies (input independent)
+      for (int p = 0; p < t.npiece && p < 2; ++p) issue(a, t, sm, p);
+    }
+    stage_meta(a, t, sm);
+    // wait for the producers of the inputs; then prefetch the next descriptor
     if (threadIdx.x == 0) {
       for (int w = 0; w < t.nwait; ++w) {
         const DevWait dw = a.waits[t.wait0 + w];
         while (ld_acquire(a.ctr + dw.ctr) < dw.val) __nanosleep(32);
       }
       if (a.trace) t_ready = globaltimer();
+      s_q[b ^ 1] = q_next;
+      if (q_next < a.n_tasks) fetch_task(&s_desc[b ^ 1], a.tasks + q_next);
     }
     __syncthreads();
     if (t.type == TASK_Y_DENSE)
-      run_y_dense(a, t, sm);
+      run_y_dense(a, t, sm, pp);
     else if (t.type == TASK_T_PLR)
-      run_t_plr(a, t, sm);
+      run_t_plr(a, t, sm, pp);
     else
-      run_y_plr(a, t, sm);
+      run_y_plr(a, t, sm, pp);
+    if (threadIdx.x == 0) asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -310,6 +350,7 @@ __global__ void __launch_bounds__(EXEC_THREADS, 3) pt_exec_kernel(ExecArgs a) {
         tr[3] = smid();
       }
     }
+    b ^= 1;
   }
 }
 

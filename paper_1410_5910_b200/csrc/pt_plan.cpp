@@ -85,16 +85,39 @@ class Builder {
         const int g = new_group();
         const int32_t term_idx = (int32_t)prog_.terms.size();
         const DevKernelPLR& kp = op_.kplr[t.kernel];
-        for (int32_t s0 = 0; s0 < ns; s0 += pp_.plr_slots_per_task) {
+        for (int32_t s0 = 0; s0 < ns;) {
+          // slots whose Vt rows fill at most one smem buffer half
+          // up to T_PIECES pieces, each a run of slots filling one buffer half
           DevTask tk{};
           tk.type = TASK_T_PLR;
           tk.r0 = s0;
-          tk.r1 = std::min<int32_t>(ns, s0 + pp_.plr_slots_per_task);
           tk.term0 = term_idx;
           tk.nterm = 1;
-          double c = 0;
-          for (int32_t s = tk.r0; s < tk.r1; ++s) c += 16.0 * op_.slots[kp.slot0 + s].cols;
-          push_task(tk, twaits, g, c);
+          tk.piece0 = (int32_t)prog_.pieces.size();
+          int32_t s1 = s0;
+          int64_t total = 0;
+          const int32_t cap = std::min(pp_.plr_slots_per_task, MAX_T_SLOTS);
+          for (int np = 0; np < pp_.t_pieces && s1 < ns && s1 - s0 < cap; ++np) {
+            DevPiece pc{};
+            pc.src = op_.slots[kp.slot0 + s1].v_off;
+            pc.f0 = s1 - s0;
+            int64_t elems = 0;
+            while (s1 < ns && s1 - s0 < cap) {
+              const int64_t c = op_.slots[kp.slot0 + s1].cols;
+              if (s1 - s0 > pc.f0 && elems + c > pp_.half_elems) break;
+              elems += c;
+              ++s1;
+            }
+            if (elems > pp_.half_elems) overflow_ = true;
+            pc.elems = (int32_t)elems;
+            pc.f1 = s1 - s0;
+            prog_.pieces.push_back(pc);
+            total += elems;
+          }
+          tk.r1 = s1;
+          tk.npiece = (int32_t)prog_.pieces.size() - tk.piece0;
+          push_task(tk, twaits, g, 16.0 * (double)total);
+          s0 = s1;
         }
         register_producer(ref(SLOT_T, dt.t_base), g);
         add_wait(waits, ref(SLOT_T, dt.t_base));
@@ -118,23 +141,57 @@ class Builder {
     const int rpt = plr ? pp_.plr_rows_per_task : pp_.dense_rows_per_task;
     for (int64_t r0 = 0; r0 < m; r0 += rpt) {
       DevTask tk{};
+      tk.piece0 = (int32_t)prog_.pieces.size();
       if (plr) {  // flat tile entries of all terms, t0 absolute, prefix column counts
         tk.ent0 = (int32_t)prog_.ents.size();
         int32_t pre = 0;
         for (size_t it = 0; it < terms.size(); ++it) {
           const DevTerm& dt = prog_.terms[term0 + it];
           const int32_t k0 = op_.kplr[dt.kernel].tile0 + (int32_t)(r0 / PLR_TILE);
+          // pieces: whole columns of this term's (contiguous) tile chunk
+          DevPiece pc{};
+          bool open = false;
           for (int32_t e = op_.tile_ptr[k0]; e < op_.tile_ptr[k0 + 1]; ++e) {
             DevTileEntry te = op_.tile_ent[e];
+            const int32_t eidx = (int32_t)prog_.ents.size() - tk.ent0;
+            for (int32_t c = 0; c < te.rank; ++c) {
+              const int64_t addr = te.u0 + (int64_t)c * te.stride;
+              if (open && pc.elems + te.stride > pp_.half_elems) {
+                prog_.pieces.push_back(pc);
+                open = false;
+              }
+              if (!open) {
+                pc = DevPiece{};
+                pc.src = addr;
+                pc.f0 = pre + c;
+                pc.e0 = eidx;
+                open = true;
+              }
+              pc.elems += te.stride;
+              pc.f1 = pre + c + 1;
+            }
             te.t0 = (int32_t)(te.t0 + dt.t_base);
             te.pre = pre;
             pre += te.rank;
             prog_.ents.push_back(te);
           }
+          if (open) prog_.pieces.push_back(pc);
         }
         tk.nent = (int32_t)prog_.ents.size() - tk.ent0;
-        if (tk.nent > MAX_TILE_ENTRIES) overflow_ = true;
+        tk.ncol = pre;
+        if (tk.nent > MAX_TILE_ENTRIES || tk.ncol > MAX_TCOLS) overflow_ = true;
+      } else {
+        for (size_t it = 0; it < terms.size(); ++it) {
+          DevPiece pc{};
+          pc.src = ((int64_t)terms[it].kernel * m + r0) * m;
+          pc.elems = (int32_t)((std::min<int64_t>(m, r0 + rpt) - r0) * m);
+          pc.f0 = (int32_t)it;
+          pc.f1 = (int32_t)it + 1;
+          if (pc.elems > pp_.half_elems) overflow_ = true;
+          prog_.pieces.push_back(pc);
+        }
       }
+      tk.npiece = (int32_t)prog_.pieces.size() - tk.piece0;
       tk.type = plr ? TASK_Y_PLR : TASK_Y_DENSE;
       tk.r0 = (int32_t)r0;
       tk.r1 = (int32_t)std::min<int64_t>(m, r0 + rpt);
@@ -228,6 +285,7 @@ class Builder {
     out.terms = prog_.terms;
     out.eyes = prog_.eyes;
     out.ents = prog_.ents;
+    out.pieces = prog_.pieces;
     out.t_elems = prog_.t_elems;
     out.term_bytes = prog_.term_bytes;
     out.algo_bytes = prog_.algo_bytes;

@@ -31,6 +31,7 @@ struct Operator {
   std::vector<DevKernelPLR> kplr;
   std::vector<int32_t> tile_ptr;
   std::vector<DevTileEntry> tile_ent;
+  std::vector<int64_t> tile_chunk;  // per (kernel, tile): offset of its U chunk
   std::vector<int32_t> nslot;  // per kernel: sum of ranks
 };
 
@@ -40,6 +41,7 @@ struct Program {
   std::vector<DevEye> eyes;
   std::vector<DevWait> waits;
   std::vector<DevTileEntry> ents;  // Y_PLR task entries (t0 absolute, pre = prefix)
+  std::vector<DevPiece> pieces;    // staged operator ranges of every task
   int n_counters = 0;
   int64_t t_elems = 0;      // size of SLOT_T needed
   int64_t term_bytes = 0;   // kernel bytes actually streamed by the terms
@@ -57,11 +59,13 @@ std::string sweep_diagonal_error(const Operator& op);
 // Program kinds.
 struct PlanParams {
   int ctas = 444;                // executor CTAs (queue-order simulation)
+  int64_t half_elems = 1024;     // complex capacity of one smem buffer half
   double task_us = 2.0;          // fixed cost per task in the simulation
   double cta_gbs = 25.0;         // streaming rate of one CTA in the simulation
   int dense_rows_per_task = 16;  // Y_DENSE rows per task
   int plr_rows_per_task = PLR_TILE;  // Y_PLR rows per task (lane per row)
   int plr_slots_per_task = 64;   // T_PLR slots per task (warp per slot)
+  int t_pieces = 2;              // buffer-half pieces per T_PLR task
 };
 
 Program build_apply_A(const Operator& op, const PlanParams& pp);

@@ -72,6 +72,20 @@ struct DevTask {
   VecRef rhs;          // Y: + rhs_coef * rhs
   double rhs_coef;
   int32_t ent0, nent;  // Y_PLR: flat tile entries of all terms (program ents array)
+  int32_t piece0, npiece;  // operator ranges staged into smem (program pieces array)
+  int32_t ncol;        // Y_PLR: flat columns of the task
+  int32_t pad2;        // 16-byte multiple (cp.async copies of the descriptor)
+};
+
+// One contiguous operator range a task stages into a smem buffer half with a
+// TMA bulk copy.  Y_PLR: whole rank columns [f0, f1) of the task's flat column
+// list, e0 = task-relative entry holding f0.  T_PLR: slots [f0, f1) of the
+// task.  Y_DENSE: rows r0..r1 of term f0's kernel.
+struct DevPiece {
+  int64_t src;     // element offset into the operator pool (dense or factors)
+  int32_t elems;
+  int32_t f0, f1;
+  int32_t e0;
 };
 
 // PLR storage on the device.  For each leaf the factors are stored as
@@ -88,8 +102,10 @@ struct DevSlot {     // one Vt row, for the t-phase
   int32_t col_off, cols;
 };
 
-constexpr int PLR_TILE = 32;  // rows of a Y_PLR task (one per lane)
+constexpr int PLR_TILE = 16;           // rows of a Y_PLR task
 constexpr int MAX_TILE_ENTRIES = 256;  // leaf entries of one Y_PLR task (all terms)
+constexpr int MAX_TCOLS = 1024;        // flat rank columns of one Y_PLR task
+constexpr int MAX_T_SLOTS = 512;       // Vt rows of one T_PLR task
 
 struct DevKernelPLR {
   int32_t leaf0, nleaf;      // into the leaf table
@@ -98,8 +114,10 @@ struct DevKernelPLR {
   int32_t pad;               //                                  tile_ptr[tile0+t+1])
 };
 
-// One leaf as seen from one PLR_TILE-row tile: lanes [lo, hi) of the tile
-// lie inside the leaf; lane l reads U column c at u0 + c*stride + (l - lo).
+// One leaf as seen from one PLR_TILE-row tile.  U is stored tile-major: for
+// each tile, each leaf meeting it, each rank column, the tile's rows of that
+// column (hi - lo values).  Tile row r (lo <= r < hi) of column c is at
+// u0 + c*stride + (r - lo), stride = hi - lo, u0 an absolute factor offset.
 struct DevTileEntry {
   int64_t u0;
   int32_t t0;      // first slot of the leaf (kernel-relative in the operator table,

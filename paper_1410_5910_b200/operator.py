@@ -192,6 +192,14 @@ class DeviceOperator:
                                        self.stream()), "pt_apply_M")
         return self._ret(z, host)
 
+    def apply_AM(self, x, n_it=2, out=None):
+        """w = M^-1 (A x) in one fused launch (one GMRES iteration's operator work)."""
+        xd, host = self._dev_vec(x)
+        w = self._out(out, host)
+        nat.check(nat.lib().pt_apply_AM(self._h, xd.data_ptr(), w.data_ptr(), int(n_it),
+                                        self.stream()), "pt_apply_AM")
+        return self._ret(w, host)
+
     def gs_sweep(self, rhs, u_in, out=None):
         rd, host = self._dev_vec(rhs, "rhs")
         ud, _ = self._dev_vec(u_in, "u_in")
@@ -235,6 +243,12 @@ class DeviceOperator:
         nat.check(nat.lib().pt_exec_stats(self._h, C.byref(ms), C.byref(n), C.byref(b)),
                   "pt_exec_stats")
         return float(ms.value), int(n.value), int(b.value)
+
+    def exec_info(self):
+        """{'grid': CTAs, 'smem': bytes per CTA, 'half_elems': staging half (complex)}."""
+        g, sm, hf = C.c_int32(), C.c_int64(), C.c_int64()
+        nat.check(nat.lib().pt_exec_info(self._h, C.byref(g), C.byref(sm), C.byref(hf)), "info")
+        return {"grid": int(g.value), "smem": int(sm.value), "half_elems": int(hf.value)}
 
     def bytes_apply_A(self):
         return int(nat.lib().pt_bytes_apply_A(self._h))

@@ -76,6 +76,27 @@ def test_applies_bitwise_repeatable_and_linear(cuda_ok, name):
     assert np.abs(combo - split).max() <= 1e-13 * np.abs(combo).max()
 
 
+def _fused_matches_separate(op, x):
+    import torch
+    xd = torch.from_numpy(np.asarray(x)).cuda()
+    ref = op.apply_M(op.apply_A(xd))
+    for _ in range(8):  # a scheduling race would show up as a mismatch
+        assert torch.equal(op.apply_AM(xd), ref)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fused_iteration_equals_separate_applies(cuda_ok, name):
+    meta, arr, op = get(name)
+    _fused_matches_separate(op, arr["probe_x"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c3r", "c2", "c3"])
+def test_fused_iteration_equals_separate_applies_large(cuda_ok, name):
+    meta, arr, op = get(name, big=True)
+    _fused_matches_separate(op, arr["probe_x"])
+
+
 @pytest.mark.parametrize("name", FIXTURES)
 def test_gmres_matches_reference(cuda_ok, name):
     meta, arr, op = get(name)

@@ -56,6 +56,6 @@ for name in sys.argv[1:]:
           f"A {tA*1e3:.1f} us {bA/tA/1e6:.0f} GB/s ({bA/tA/1e6/PEAK:.2f}) | "
           f"M {tM*1e3:.1f} us {bM/tM/1e6:.0f} GB/s ({bM/tM/1e6/PEAK:.2f}) | "
           f"gmres {tg:.2f} ms it={k} ref_it={meta['solves'][0]['iterations']} "
-          f"per-it {tg/max(k,1):.3f} ms cpu_ref_gmres={meta['solves'][0]['stage_seconds'].get('gmres')}",
+          f"per-it {tg/max(k,1):.3f} ms {op.exec_info()}",
           flush=True)
     op.close()
