@@ -252,13 +252,25 @@ def run_ours(args):
     upload_s = time.perf_counter() - t0
     N = op.N
     tol, max_iter, n_it = meta["gmres_tol"], meta["gmres_max_iter"], meta["n_it"]
-    b = torch.from_numpy(np.array(arr["rhs"][0])).to(f"cuda:{local}")
+    from paper_1410_5910_b200.replicas import gather_counts, max_over_ranks, shard
+    nrhs = int(np.asarray(arr["rhs"]).shape[0])
+    # multi-RHS workloads shard their sources across ranks; single-RHS ones
+    # run one replica per rank (no collective on the data path)
+    mine = list(shard(nrhs, world, rank)) if nrhs > 1 else [0]
+    rhs_dev = [torch.from_numpy(np.array(arr["rhs"][s])).to(f"cuda:{local}") for s in mine]
+    b = rhs_dev[0]
     x = torch.empty_like(b)
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=f"cuda:{local}")
     stream = torch.cuda.current_stream()
 
+    def step():
+        rep = None
+        for bs in rhs_dev:
+            _, rep = op.gmres(bs, rel_tol=tol, max_iter=max_iter, n_it=n_it, out=x)
+        return rep
+
     for _ in range(args.warmup):
-        op.gmres(b, rel_tol=tol, max_iter=max_iter, n_it=n_it, out=x)
+        step()
     torch.cuda.synchronize()
 
     def barrier():
@@ -277,7 +289,7 @@ def run_ours(args):
             flush.zero_()  # evict L2 (outside the timed interval)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _, rep = op.gmres(b, rel_tol=tol, max_iter=max_iter, n_it=n_it, out=x)
+            rep = step()
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -295,7 +307,7 @@ def run_ours(args):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        op.gmres(b, rel_tol=tol, max_iter=max_iter, n_it=n_it, out=x)
+        step()
         e1.record(stream)
         e1.synchronize()
         instr_ms.append(e0.elapsed_time(e1))
@@ -305,25 +317,28 @@ def run_ours(args):
 
     # end to end through the host-buffer C-ABI call (pt_gmres_host): H2D of b
     # from pinned memory, the solve, D2H of x, all inside the timed interval
-    b_host = torch.from_numpy(np.array(arr["rhs"][0])).pin_memory()
-    x_host = torch.empty_like(b_host).pin_memory()
+    b_host = [torch.from_numpy(np.array(arr["rhs"][s])).pin_memory() for s in mine]
+    x_host = torch.empty_like(b_host[0]).pin_memory()
     e2e_ms = []
-    op.gmres_host(b_host, x_host, rel_tol=tol, max_iter=max_iter, n_it=n_it)
+
+    def step_host():
+        for bh in b_host:
+            op.gmres_host(bh, x_host, rel_tol=tol, max_iter=max_iter, n_it=n_it)
+
+    step_host()
     for _ in range(args.steps):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        op.gmres_host(b_host, x_host, rel_tol=tol, max_iter=max_iter, n_it=n_it)
+        step_host()
         e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
     e2e_total = float(sum(e2e_ms))
-
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_total = float(t[0]), float(t[1])
+    dev = f"cuda:{local}"
+    total_ms = max_over_ranks(total_ms, dev)
+    e2e_total = max_over_ranks(e2e_total, dev)
+    solves_per_step = gather_counts(len(mine), dev)
 
     # parity of the timed solve vs the reference's own solution (cheap check)
     nt, m = meta["nt"], meta["m"]
@@ -340,8 +355,8 @@ def run_ours(args):
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get(name)
-    per_step_bytes = exec_bytes / max(args.steps, 1)  # algorithmic bytes per solve
-    value = total_ms / (args.steps * world)
+    per_step_bytes = exec_bytes / max(args.steps * len(mine), 1)  # algorithmic bytes per solve
+    value = total_ms / (args.steps * solves_per_step)
     line = {
         "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": False,
@@ -362,13 +377,15 @@ def run_ours(args):
             "kernel_share_of_step": exec_ms / instr_total if instr_total > 0 else None,
             "measured": "per-launch CUDA events in an instrumented pass of the same K solves",
         },
-        "solve": {"per_iteration_ms": (total_ms / args.steps) / max(k, 1),
-                  "solve_gbs": per_step_bytes / (total_ms / args.steps * 1e-3) / 1e9,
-                  "solve_frac": per_step_bytes / (total_ms / args.steps * 1e-3) / 1e9 / peak,
+        "solve": {"per_iteration_ms": (total_ms / args.steps / len(mine)) / max(k, 1),
+                  "solves_per_step": solves_per_step,
+                  "solve_gbs": per_step_bytes / (total_ms / args.steps / len(mine) * 1e-3) / 1e9,
+                  "solve_frac": per_step_bytes / (total_ms / args.steps / len(mine) * 1e-3) / 1e9
+                  / peak,
                   "algorithmic_bytes_per_solve": per_step_bytes,
                   "upload_s": upload_s, "offline_host_s": meta.get("offline_seconds")},
-        "e2e": {"value": e2e_total / (args.steps * world), "unit": "ms",
-                "h2d_bytes_per_step": N * 16, "d2h_bytes_per_step": N * 16,
+        "e2e": {"value": e2e_total / (args.steps * solves_per_step), "unit": "ms",
+                "h2d_bytes_per_step": N * 16 * len(mine), "d2h_bytes_per_step": N * 16 * len(mine),
                 "api": "pt_gmres_host (C ABI, pinned host b/x)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
