@@ -100,7 +100,11 @@ typedef struct {
  * solver.py:110-129, built by assemble_polarized + split_DR,
  * trace_system.py:368-524).  dense: n_kernels*m*m complex (host) or NULL;
  * leaves/factors: PLR tables (host) or NULL.  perm is sweep_permutation
- * (trace_system.py:353-365) in natural block-row indices. */
+ * (trace_system.py:353-365) in natural block-row indices.
+ * device = PT_DEVICE_HOST builds the host-side tables only (B200 launch
+ * shape assumed, dense may be NULL): such a handle answers pt_plan_stats and
+ * pt_exec_info, everything else returns PT_EINVAL. */
+#define PT_DEVICE_HOST (-1) /* pt_create device: plan-only handle, no GPU */
 int pt_create(const pt_layout *layout, const pt_entry *entries,
               int64_t n_entries, const int64_t *perm, const double *dense,
               const pt_leaf *leaves, int64_t n_leaves, const double *factors,
@@ -178,9 +182,14 @@ int pt_exec_stats(pt_handle *h, double *total_ms, int64_t *launches,
 
 /* Run one operator program (kind 0 = A-apply, 1 = n_it-sweep preconditioner,
  * 2 = fused A->M iteration, 3 = one sweep with u_in = in) with a per-task
- * timeline: rec[12*q ...] = {type, out slot, out offset, r0, r1, terms,
- * t_grab, t_ready, t_done (globaltimer ns), SM id, kernel (T tasks), group}
- * for every task q in queue order.  Profiling aid; synchronises. */
+ * timeline: rec[PT_TRACE_WORDS*q ...] = {type, out slot, out offset, r0, r1,
+ * terms, t_grab, t_ready (dependencies met), t_done (globaltimer ns), SM id |
+ * CTA index << 16,
+ * t_consumers_start, group, t_staged, pieces, t_issue[8] (producer issued
+ * operator piece k), t_landed[8] (consumers saw piece k), consumer cycles
+ * waiting for pieces, consumer cycles in per-piece barriers} for every task q in
+ * queue order (0 = not recorded).  Profiling aid; synchronises. */
+#define PT_TRACE_WORDS 32
 int pt_trace_program(pt_handle *h, int32_t kind, int32_t n_it, const double *in,
                      double *out, int64_t *rec, int64_t cap, int64_t *n_out);
 
@@ -188,6 +197,15 @@ int pt_trace_program(pt_handle *h, int32_t kind, int32_t n_it, const double *in,
  * the complex capacity of one operator staging buffer half. */
 int pt_exec_info(const pt_handle *h, int32_t *grid, int64_t *smem_bytes,
                  int64_t *half_elems);
+
+/* Host-side plan of one program (kind as in pt_trace_program) without
+ * running it: stats[0..11] = {tasks, T_PLR tasks, Y_PLR tasks, Y_DENSE tasks,
+ * operator pieces, metadata items, counters, algorithmic bytes, staged
+ * operator bytes, max terms of a task, max pieces of a task, max items of a
+ * task}.  PT_EINVAL (pt_last_error says why) if a task exceeds what the
+ * executor stages.  Needs no GPU. */
+#define PT_PLAN_STATS 12
+int pt_plan_stats(pt_handle *h, int32_t kind, int32_t n_it, int64_t *stats);
 
 /* ---- misc ----------------------------------------------------------------*/
 const char *pt_last_error(void);

@@ -17,6 +17,7 @@ LIB_PATH = Path(os.environ.get("PT_B200_LIB", _HERE / "libpt_b200.so"))
 
 PT_OK, PT_EINVAL, PT_ECUDA, PT_ENONFINITE = 0, -1, -2, -3
 PT_KERNEL_DENSE, PT_KERNEL_PLR = 0, 1
+PT_DEVICE_HOST = -1
 FLAGS = {0: "converged", 1: "breakdown", 2: "stagnation", 3: "maxiter"}
 
 
@@ -73,6 +74,7 @@ _SIGS = {
                                 C.POINTER(C.c_int64)]),
     "pt_trace_program": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP, C.POINTER(C.c_int64),
                                    C.c_int64, C.POINTER(C.c_int64)]),
+    "pt_plan_stats": (C.c_int, [_VP, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
     "pt_exec_info": (C.c_int, [_VP, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64)]),
     "pt_last_error": (C.c_char_p, []),

@@ -56,9 +56,15 @@ struct DevProgram {
   DevWait* waits = nullptr;
   DevTileEntry* ents = nullptr;
   DevPiece* pieces = nullptr;
+  DevItem* items = nullptr;
+  int4* blob = nullptr;        // per-task metadata blobs (queue order)
+  int64_t* blob_off = nullptr;  // task q: blob[blob_off[q] .. blob_off[q + 1])
   ~DevProgram() {
+    cudaFree(blob);
+    cudaFree(blob_off);
     cudaFree(ents);
     cudaFree(pieces);
+    cudaFree(items);
     cudaFree(tasks);
     cudaFree(terms);
     cudaFree(eyes);
@@ -108,6 +114,7 @@ struct pt_gmres_ws {
 
 struct pt_handle {
   int device = 0;
+  bool host_only = false;  // PT_DEVICE_HOST: plan tables only
   Operator op;
   std::string sweep_err;
   PlanParams pp;
@@ -125,7 +132,11 @@ struct pt_handle {
   int ctr_cap = 0;
   int grid = 0;
   size_t smem = 0;
-  int64_t src_cap = 0;
+  int64_t src_cap = 0;     // complex elements of a task slot's vector staging
+  int64_t item_cap = 0;    // items of a task slot
+  int64_t blob_cap = 0;    // bytes of a task slot's metadata blob area
+  int64_t slot_bytes = 0;  // bytes of one task slot
+  int n_stages = 4;        // operator ring stages
   std::unique_ptr<pt_gmres_ws> gws;
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
@@ -231,6 +242,11 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
       op.kernel_bytes[k] += 16 * L.rank * (L.rows + L.cols);
       if (L.rank > 0) kl.push_back(&L);
     }
+    // slots ordered by column band: a T task's run of slots then reads a
+    // narrow range of the source vector
+    std::stable_sort(kl.begin(), kl.end(), [](const pt_leaf* a, const pt_leaf* b) {
+      return a->col_off != b->col_off ? a->col_off < b->col_off : a->row_off < b->row_off;
+    });
     // Vt region
     align8();
     int32_t slot = 0;
@@ -289,6 +305,7 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
   }
   if (op.tile_ent.empty()) op.tile_ent.push_back(DevTileEntry{});
   if (blob.empty()) blob.push_back(make_double2(0.0, 0.0));
+  if (h->host_only) return 0;
   int rc;
   if ((rc = upload(&h->fac, blob))) return rc;
   if ((rc = upload(&h->slots, op.slots))) return rc;
@@ -308,6 +325,70 @@ int ensure_slot(pt_handle* h, int s, int64_t elems) {
   return 0;
 }
 
+// Per-task metadata blobs, in queue order, so a producer warp fetches a
+// task's whole description with one bulk copy:
+//   [DevTask][DevPiece x npiece][DevTerm x nterm][DevEye x neye]
+//   [DevWait x nwait][DevRun x nrun][DevItem x nitem]
+// each section 16-byte aligned.  In the blob copy of the DevTask, piece0 /
+// term0 / eye0 / wait0 / run0 / item0 are byte offsets of the sections and
+// q is the queue index.
+int64_t blob_bytes_max(int64_t item_cap) {
+  auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
+  return al(sizeof(DevTask)) + al(EXEC_PIECES * sizeof(DevPiece)) + al(EXEC_TERMS * sizeof(DevTerm)) +
+         al(EXEC_EYES * sizeof(DevEye)) + al(EXEC_WAITS * sizeof(DevWait)) +
+         al(EXEC_RUNS * sizeof(DevRun)) + al(item_cap * (int64_t)sizeof(DevItem));
+}
+
+void build_blobs(const Program& pg, std::vector<int4>& blob, std::vector<int64_t>& off,
+                 int64_t* max_bytes) {
+  std::vector<char> b;
+  off.assign(pg.tasks.size() + 1, 0);
+  *max_bytes = 0;
+  auto put = [&](const void* p, size_t n) {
+    const int32_t at = (int32_t)b.size();
+    b.insert(b.end(), (const char*)p, (const char*)p + n);
+    while (b.size() % 16) b.push_back(0);
+    return at;
+  };
+  for (size_t q = 0; q < pg.tasks.size(); ++q) {
+    const DevTask& t = pg.tasks[q];
+    b.clear();
+    DevTask d = t;
+    put(&d, sizeof(DevTask));
+    d.piece0 = put(pg.pieces.data() + t.piece0, (size_t)t.npiece * sizeof(DevPiece));
+    d.term0 = put(pg.terms.data() + t.term0, (size_t)t.nterm * sizeof(DevTerm));
+    d.eye0 = put(pg.eyes.data() + t.eye0, (size_t)t.neye * sizeof(DevEye));
+    d.wait0 = put(pg.waits.data() + t.wait0, (size_t)t.nwait * sizeof(DevWait));
+    d.run0 = put(pg.runs.data() + t.run0, (size_t)t.nrun * sizeof(DevRun));
+    d.item0 = put(pg.items.data() + t.item0, (size_t)t.nitem * sizeof(DevItem));
+    d.q = (int32_t)q;
+    std::memcpy(b.data(), &d, sizeof(DevTask));
+    *max_bytes = std::max<int64_t>(*max_bytes, (int64_t)b.size());
+    const size_t at = blob.size();
+    blob.resize(at + b.size() / 16);
+    std::memcpy(blob.data() + at, b.data(), b.size());
+    off[q + 1] = (int64_t)blob.size();
+  }
+}
+
+// Every task of a program fits the executor's task slot (the handle sized the
+// slots from the operator; a program that does not fit is rejected).
+int check_slots(const pt_handle* h, const Program& pg) {
+  for (const DevTask& t : pg.tasks) {  // what one task slot stages
+    int64_t vec = 0;
+    if (t.type == TASK_T_PLR) vec = 2 * (t.c1 - t.c0);  // both sources of a merged term
+    if (t.type == TASK_Y_PLR) vec = t.nitem;
+    if (t.type == TASK_Y_DENSE) vec = 2 * (int64_t)t.nterm * h->op.m;
+    const int rows = t.type == TASK_Y_DENSE ? DENSE_RT_MAX : EXEC_EPI;
+    if (vec > h->src_cap || t.nitem > h->item_cap || t.nterm > EXEC_TERMS ||
+        t.neye > EXEC_EYES || t.npiece > EXEC_PIECES || t.nwait > EXEC_WAITS ||
+        t.nrun > EXEC_RUNS ||
+        (t.type != TASK_T_PLR && t.r1 - t.r0 > rows))
+      return fail(PT_EINVAL, "a task stages more than the executor's task slot holds");
+  }
+  return 0;
+}
+
 int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** out) {
   const std::string key = kind + std::to_string(n_it);
   auto it = h->progs.find(key);
@@ -324,9 +405,8 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
     p->host = build_gs_sweep(h->op, h->pp);
   else
     p->host = build_A_then_M(h->op, n_it, h->pp);
-  if (p->host.overflow)
-    return fail(PT_EINVAL, "a PLR row tile meets more leaves than the executor stages (" +
-                               std::to_string(MAX_TILE_ENTRIES) + ")");
+  if (!p->host.overflow.empty()) return fail(PT_EINVAL, p->host.overflow);
+  if (int rc = check_slots(h, p->host)) return rc;
   int rc;
   if ((rc = upload(&p->tasks, p->host.tasks))) return rc;
   if ((rc = upload(&p->terms, p->host.terms))) return rc;
@@ -334,6 +414,16 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
   if ((rc = upload(&p->waits, p->host.waits))) return rc;
   if ((rc = upload(&p->ents, p->host.ents))) return rc;
   if ((rc = upload(&p->pieces, p->host.pieces))) return rc;
+  if ((rc = upload(&p->items, p->host.items))) return rc;
+  {
+    std::vector<int4> blob;
+    std::vector<int64_t> off;
+    int64_t mx = 0;
+    build_blobs(p->host, blob, off, &mx);
+    if (mx > h->blob_cap) return fail(PT_EINVAL, "a task's metadata exceeds the executor's task slot");
+    if ((rc = upload(&p->blob, blob))) return rc;
+    if ((rc = upload(&p->blob_off, off))) return rc;
+  }
   for (int s : {SLOT_Y, SLOT_U1, SLOT_U2, SLOT_PRE, SLOT_T})
     if ((rc = ensure_slot(h, s, p->host.slot_elems[s]))) return rc;
   if (p->host.n_counters + 1 > h->ctr_cap) {
@@ -377,8 +467,14 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.tile_ent = h->tile_ent;
   a.ents = p->ents;
   a.pieces = p->pieces;
+  a.items = p->items;
+  a.blob = p->blob;
+  a.blob_off = p->blob_off;
+  a.blob_cap = h->blob_cap;
   a.half_elems = h->pp.half_elems;
   a.src_cap = h->src_cap;
+  a.slot_bytes = h->slot_bytes;
+  a.n_stages = h->n_stages;
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
   a.stop = stop;
@@ -538,12 +634,16 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (!layout || !out || (n_entries > 0 && !entries) || !perm)
     return fail(PT_EINVAL, "null argument to pt_create");
   *out = nullptr;
-  int ndev = 0;
-  CK(cudaGetDeviceCount(&ndev));
-  if (device < 0 || device >= ndev) return fail(PT_EINVAL, "no such CUDA device");
-  DeviceGuard guard(device);
+  const bool host_only = device == PT_DEVICE_HOST;
+  if (!host_only) {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(PT_EINVAL, "no such CUDA device");
+  }
+  std::unique_ptr<DeviceGuard> guard(host_only ? nullptr : new DeviceGuard(device));
   std::unique_ptr<pt_handle> h(new pt_handle());
   h->device = device;
+  h->host_only = host_only;
   Operator& op = h->op;
   op.m = layout->m;
   op.nb = layout->n_block_rows;
@@ -564,7 +664,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   int rc;
   if (op.fmt == PT_KERNEL_DENSE) {
     op.kernel_bytes.assign(op.nk, 16 * op.m * op.m);
-    if (op.nk > 0) {
+    if (op.nk > 0 && !host_only) {
       if (!dense) return fail(PT_EINVAL, "dense kernel array missing");
       const size_t bytes = (size_t)op.nk * op.m * op.m * sizeof(double2);
       CK(cudaMalloc(&h->dense, bytes));
@@ -574,62 +674,131 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     if (n_leaves > 0 && (!leaves || !factors)) return fail(PT_EINVAL, "PLR tables missing");
     if ((rc = build_plr_tables(h.get(), leaves, n_leaves, factors, n_factor_complex))) return rc;
   }
-  // Shared memory per CTA: [two operator buffer halves][source / t staging]
-  // [partials][task metadata].  The halves take what is left after the fixed
-  // part at the largest CTA count per SM (<= 3, or PT_CTAS_PER_SM) for which
-  // one half still holds the largest contiguous unit a task stages (a dense
-  // row, a Vt row).
-  h->src_cap = std::max<int64_t>(op.m, MAX_TCOLS);
-  const size_t meta = std::max(MAX_TILE_ENTRIES * sizeof(DevTileEntry), MAX_T_SLOTS * sizeof(DevSlot));
-  const size_t fixed = ((size_t)h->src_cap + EXEC_THREADS) * sizeof(double2) + meta;
+  // Shared memory per CTA: [EXEC_STAGES operator ring stages][EXEC_TSLOTS task
+  // slots: descriptor, items, staged vectors, epilogue rows, term scales]
+  // [consumer partials].  The stages take what is left after the fixed part
+  // at one CTA per SM (the loop admits more if EXEC_THREADS shrinks) for which one
+  // stage still holds the largest contiguous unit a task stages (a dense
+  // kernel row, a Vt row, a tile column).
   int64_t need = op.m;  // dense: one kernel row
   if (op.fmt == PT_KERNEL_PLR) {
     need = PLR_TILE;
     for (const DevSlot& sl : op.slots) need = std::max<int64_t>(need, sl.cols);
+    // a Y_PLR task stages one item and one t value per rank column meeting its
+    // row tile (all terms; independent of the stage size), a T_PLR task one
+    // item per Vt row (<= MAX_T_SLOTS) and a source slice (<= tcols_cap)
+    PlanParams probe;
+    probe.half_elems = (int64_t)1 << 30;
+    int64_t ycols = 0;
+    for (const Program& pg : {build_apply_A(op, probe), build_apply_M(op, 2, probe),
+                              build_gs_sweep(op, probe)})
+      for (const DevTask& t : pg.tasks)
+        if (t.type == TASK_Y_PLR) ycols = std::max<int64_t>(ycols, t.nitem);
+    int64_t widest = 0;
+    for (const DevSlot& sl : op.slots) widest = std::max<int64_t>(widest, sl.cols);
+    h->item_cap = (std::max<int64_t>(ycols, MAX_T_SLOTS) + 7) / 8 * 8;
+    h->pp.tcols_cap = std::max<int64_t>(widest, std::min<int64_t>(op.m, MAX_TCOLS));
+    // Y: one t value per column; T: both sources of a merged term's slice
+    h->src_cap = std::max<int64_t>(h->item_cap, 2 * h->pp.tcols_cap);
+    h->pp.item_cap = h->item_cap;
+  } else {
+    // a dense Y task stages one source vector per kernel term: the most terms
+    // any program's task carries (the plan's term structure does not depend
+    // on the stage size)
+    PlanParams probe;
+    probe.half_elems = (int64_t)1 << 30;
+    probe.dense_rows_per_task = 1;
+    int64_t terms = 1;
+    for (const Program& pg : {build_apply_A(op, probe), build_apply_M(op, 2, probe),
+                              build_gs_sweep(op, probe)})
+      for (const DevTask& t : pg.tasks) terms = std::max<int64_t>(terms, t.nterm);
+    h->src_cap = 2 * terms * op.m;  // both sources of every term
+    h->item_cap = 0;
   }
-  int smem_sm = 0, smem_blk = 0;
-  CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
-  CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  int target = 3;
-  if (const char* e = std::getenv("PT_CTAS_PER_SM")) target = std::max(1, std::min(4, std::atoi(e)));
+  h->blob_cap = (blob_bytes_max(h->item_cap) + 127) / 128 * 128;
+  h->slot_bytes =
+      h->blob_cap +
+      (h->src_cap + EXEC_EPI * EXEC_EPI_SRC + EXEC_TERMS + EXEC_EYES) * (int64_t)sizeof(double2) +
+      EXEC_SRCS * (int64_t)sizeof(void*);
+  h->slot_bytes = (h->slot_bytes + 127) / 128 * 128;
+  // + the consumers' partials
+  const size_t fixed = (size_t)EXEC_TSLOTS * h->slot_bytes + EXEC_CONSUMERS * sizeof(double2);
+  // B200 figures for a host-only handle; the device's own otherwise
+  int smem_sm = 233472, smem_blk = 232448, reserved = 1024, nsm = 148;
   cudaFuncAttributes fa{};
-  CK(cudaFuncGetAttributes(&fa, pt_exec_kernel));
-  int reserved = 1024;
-  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+  fa.sharedSizeBytes = 512;
+  if (!host_only) {
+    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+    CK(cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaFuncGetAttributes(&fa, pt_exec_kernel));
+    cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+  }
+  int target = 1;  // one CTA of EXEC_THREADS per SM
+  // ring: 3 stages (PT_STAGES overrides, 2..8; fewer if a stage would not
+  // hold `need`).  Items address a stage with 16-bit offsets.
+  int max_stages = 3;
+  if (const char* e = std::getenv("PT_STAGES"))
+    max_stages = std::max(2, std::min(EXEC_MAX_STAGES, std::atoi(e)));
   int64_t half = 0;
-  for (int c = target; c >= 1; --c) {
+  int ctas_sm = 1, stages = 2;
+  for (int c = target; c >= 1 && half < need; --c) {
+    ctas_sm = c;
     const int64_t per_cta =
         std::min<int64_t>(smem_sm / c - reserved - (int64_t)fa.sharedSizeBytes - 128, smem_blk);
-    const int64_t hb = (per_cta - (int64_t)fixed) / 2;
-    half = hb > 0 ? (hb / (int64_t)sizeof(double2)) / 8 * 8 : 0;
-    if (half >= need) break;
+    for (stages = max_stages; stages >= 2; --stages) {
+      const int64_t hb = (per_cta - (int64_t)fixed) / stages;
+      half = hb > 0 ? std::min<int64_t>(65528, (hb / (int64_t)sizeof(double2)) / 8 * 8) : 0;
+      if (half >= need) break;
+    }
   }
   if (half < need) return fail(PT_EINVAL, "block size too large for the executor's shared memory");
   h->pp.half_elems = half;
-  h->smem = 2 * (size_t)half * sizeof(double2) + fixed;
-  CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)h->smem));
-  int nsm = 0, occ = 0;
-  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_exec_kernel, EXEC_THREADS, h->smem));
-  if (occ < 1) return fail(PT_EINVAL, "executor kernel does not fit on an SM");
-  h->grid = nsm * occ;
+  h->n_stages = stages;
+  h->smem = (size_t)stages * half * sizeof(double2) + fixed;
+  if (host_only) {
+    h->grid = nsm * ctas_sm;
+  } else {
+    // the attribute is per function, shared by every handle: it only grows,
+    // so a handle with a smaller budget never caps a larger one's launches
+    static std::atomic<int> attr_max{0};
+    int cur = attr_max.load();
+    while ((int)h->smem > cur && !attr_max.compare_exchange_weak(cur, (int)h->smem)) {
+    }
+    CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            std::max(cur, (int)h->smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_exec_kernel, EXEC_THREADS, h->smem));
+    if (occ < 1) return fail(PT_EINVAL, "executor kernel does not fit on an SM");
+    h->grid = nsm * occ;
+  }
   h->pp.ctas = h->grid;
+  // (a PLR operator's Y_DENSE tasks carry no kernel term: identity/rhs rows)
   h->pp.dense_rows_per_task =
-      (int)std::max<int64_t>(1, std::min<int64_t>(DENSE_RT_MAX, half / std::max<int64_t>(op.m, 1)));
+      op.fmt == PT_KERNEL_PLR
+          ? DENSE_RT_MAX
+          : (int)std::max<int64_t>(1, std::min<int64_t>(DENSE_RT_MAX, half / std::max<int64_t>(op.m, 1)));
   h->pp.plr_rows_per_task = PLR_TILE;
   h->pp.plr_slots_per_task = MAX_T_SLOTS;
+  if (op.fmt == PT_KERNEL_DENSE) h->pp.item_cap = 0;
+  h->pp.t_pieces = 4;
   if (const char* e = std::getenv("PT_DENSE_ROWS"))
     h->pp.dense_rows_per_task = std::max(1, std::min(DENSE_RT_MAX, std::atoi(e)));
   if (const char* e = std::getenv("PT_T_SLOTS")) h->pp.plr_slots_per_task = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_T_PIECES")) h->pp.t_pieces = std::max(1, std::atoi(e));
-  CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
+  if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
+    h->pp.t_pieces_chain = std::max(1, std::atoi(e));
+  if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
   *out = h.release();
   return 0;
 }
 
 int pt_destroy(pt_handle* h) {
   if (!h) return 0;
+  if (h->host_only) {
+    delete h;
+    return 0;
+  }
   DeviceGuard guard(h->device);
   cudaDeviceSynchronize();
   delete h;
@@ -637,6 +806,7 @@ int pt_destroy(pt_handle* h) {
 }
 
 int pt_apply_A(pt_handle* h, const double* x, double* y, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !x || !y) return fail(PT_EINVAL, "null argument");
   DeviceGuard guard(h->device);
   DevProgram* p;
@@ -649,6 +819,7 @@ int pt_apply_A(pt_handle* h, const double* x, double* y, pt_stream stream) {
 }
 
 int pt_apply_M(pt_handle* h, const double* r, double* z, int32_t n_it, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !r || !z) return fail(PT_EINVAL, "null argument");
   if (n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
   if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
@@ -663,6 +834,7 @@ int pt_apply_M(pt_handle* h, const double* r, double* z, int32_t n_it, pt_stream
 }
 
 int pt_apply_AM(pt_handle* h, const double* x, double* w, int32_t n_it, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !x || !w) return fail(PT_EINVAL, "null argument");
   if (n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
   if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
@@ -678,6 +850,7 @@ int pt_apply_AM(pt_handle* h, const double* x, double* w, int32_t n_it, pt_strea
 
 int pt_gs_sweep(pt_handle* h, const double* rhs, const double* u_in, double* u_out,
                 pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !rhs || !u_in || !u_out) return fail(PT_EINVAL, "null argument");
   if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
   DeviceGuard guard(h->device);
@@ -889,6 +1062,7 @@ extern "C" {
 
 int pt_gmres(pt_handle* h, const double* b, double* x, const pt_gmres_config* cfg,
              pt_report* report, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !b || !x) return fail(PT_EINVAL, "null argument");
   int rc = check_cfg(cfg);
   if (rc) return rc;
@@ -907,6 +1081,7 @@ int pt_gmres(pt_handle* h, const double* b, double* x, const pt_gmres_config* cf
 
 int pt_gmres_host(pt_handle* h, const double* b_host, double* x_host, const pt_gmres_config* cfg,
                   pt_report* report, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !b_host || !x_host) return fail(PT_EINVAL, "null argument");
   int rc = check_cfg(cfg);
   if (rc) return rc;
@@ -932,6 +1107,7 @@ int pt_gmres_host(pt_handle* h, const double* b_host, double* x_host, const pt_g
 
 int pt_gmres_batch(pt_handle* h, const double* b, double* x, int32_t nrhs,
                    const pt_gmres_config* cfg, pt_report* reports, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !b || !x || nrhs < 0) return fail(PT_EINVAL, "bad argument");
   const int64_t N = h->N();
   for (int32_t r = 0; r < nrhs; ++r) {
@@ -992,6 +1168,7 @@ int pt_gmres_ws_finish(pt_gmres_ws* ws, int32_t k, double* x, pt_stream stream) 
 }
 
 int pt_exec_timing(pt_handle* h, int32_t enable) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h) return fail(PT_EINVAL, "null handle");
   DeviceGuard guard(h->device);
   double ms;
@@ -1002,6 +1179,7 @@ int pt_exec_timing(pt_handle* h, int32_t enable) {
 }
 
 int pt_exec_stats(pt_handle* h, double* total_ms, int64_t* launches, int64_t* algo_bytes) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h) return fail(PT_EINVAL, "null handle");
   DeviceGuard guard(h->device);
   CK(cudaDeviceSynchronize());
@@ -1024,6 +1202,7 @@ int pt_exec_stats(pt_handle* h, double* total_ms, int64_t* launches, int64_t* al
 
 int pt_trace_program(pt_handle* h, int32_t kind, int32_t n_it, const double* in, double* out,
                      int64_t* rec, int64_t cap, int64_t* n_out) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !in || !out || !rec || !n_out) return fail(PT_EINVAL, "null argument");
   DeviceGuard guard(h->device);
   const char* names[] = {"A", "M", "AM", "S"};
@@ -1036,9 +1215,11 @@ int pt_trace_program(pt_handle* h, int32_t kind, int32_t n_it, const double* in,
   *n_out = nt;
   if (cap < nt) return fail(PT_EINVAL, "trace buffer too small");
   CK(cudaDeviceSynchronize());
-  CK(cudaMalloc(&h->trace_buf, (size_t)std::max<int64_t>(nt, 1) * 4 * sizeof(unsigned long long)));
+  const size_t words = (size_t)std::max<int64_t>(nt, 1) * EXEC_TRACE;
+  CK(cudaMalloc(&h->trace_buf, words * sizeof(unsigned long long)));
+  CK(cudaMemset(h->trace_buf, 0, words * sizeof(unsigned long long)));
   rc = run_program(h, p, (const double2*)in, (double2*)out, (const double2*)in, 0);
-  std::vector<unsigned long long> tr((size_t)nt * 4);
+  std::vector<unsigned long long> tr(words);
   cudaError_t e1 = cudaDeviceSynchronize();
   cudaError_t e2 = cudaMemcpy(tr.data(), h->trace_buf, tr.size() * sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost);
@@ -1049,20 +1230,66 @@ int pt_trace_program(pt_handle* h, int32_t kind, int32_t n_it, const double* in,
   CK(e2);
   for (int64_t q = 0; q < nt; ++q) {
     const DevTask& t = p->host.tasks[q];
-    int64_t* r = rec + 12 * q;
+    const unsigned long long* w = tr.data() + EXEC_TRACE * q;
+    int64_t* r = rec + PT_TRACE_WORDS * q;
     r[0] = t.type;
     r[1] = t.out.slot;
     r[2] = t.out.off;
     r[3] = t.r0;
     r[4] = t.r1;
     r[5] = t.nterm;
-    r[6] = (int64_t)tr[4 * q + 0];
-    r[7] = (int64_t)tr[4 * q + 1];
-    r[8] = (int64_t)tr[4 * q + 2];
-    r[9] = (int64_t)tr[4 * q + 3];
-    r[10] = t.type == TASK_T_PLR ? p->host.terms[t.term0].kernel : -1;
+    r[6] = (int64_t)w[0];   // grabbed
+    r[7] = (int64_t)w[1];   // dependencies satisfied
+    r[8] = (int64_t)w[2];   // done
+    r[9] = (int64_t)w[3];   // SM id | CTA index << 16
+    r[10] = (int64_t)w[4];  // consumers started
     r[11] = t.signal;
+    r[12] = (int64_t)w[5];  // vectors staged
+    r[13] = t.npiece;
+    for (int k = 0; k < 8; ++k) {
+      r[14 + k] = (int64_t)w[14 + k];  // piece k issued
+      r[22 + k] = (int64_t)w[6 + k];   // piece k landed (consumer view)
+    }
+    r[30] = (int64_t)w[22];  // consumer cycles waiting for pieces
+    r[31] = (int64_t)w[23];  // consumer cycles in the per-piece barrier
   }
+  return 0;
+}
+
+int pt_plan_stats(pt_handle* h, int32_t kind, int32_t n_it, int64_t* stats) {
+  if (!h || !stats) return fail(PT_EINVAL, "null argument");
+  if (kind < 0 || kind > 3) return fail(PT_EINVAL, "unknown program kind");
+  if (kind == 1 || kind == 2) {
+    if (n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
+    if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  }
+  if (kind == 3 && !h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  Program pg = kind == 0   ? build_apply_A(h->op, h->pp)
+               : kind == 1 ? build_apply_M(h->op, n_it, h->pp)
+               : kind == 2 ? build_A_then_M(h->op, n_it, h->pp)
+                           : build_gs_sweep(h->op, h->pp);
+  for (int i = 0; i < PT_PLAN_STATS; ++i) stats[i] = 0;
+  stats[0] = (int64_t)pg.tasks.size();
+  for (const DevTask& t : pg.tasks) {
+    stats[t.type == TASK_T_PLR ? 1 : t.type == TASK_Y_PLR ? 2 : 3] += 1;
+    stats[9] = std::max<int64_t>(stats[9], t.nterm);
+    stats[10] = std::max<int64_t>(stats[10], t.npiece);
+    stats[11] = std::max<int64_t>(stats[11], t.nitem);
+  }
+  if (int rc = check_slots(h, pg)) return rc;
+  {
+    std::vector<int4> blob;
+    std::vector<int64_t> off;
+    int64_t mx = 0;
+    build_blobs(pg, blob, off, &mx);
+    if (mx > h->blob_cap) return fail(PT_EINVAL, "a task's metadata exceeds the executor's task slot");
+  }
+  stats[4] = (int64_t)pg.pieces.size();
+  stats[5] = (int64_t)pg.items.size();
+  stats[6] = pg.n_counters;
+  stats[7] = (int64_t)pg.algo_bytes;
+  for (const DevPiece& pc : pg.pieces) stats[8] += 16 * (int64_t)pc.elems;
+  if (!pg.overflow.empty()) return fail(PT_EINVAL, pg.overflow);
   return 0;
 }
 

@@ -7,8 +7,24 @@
 
 namespace pt {
 
-constexpr int EXEC_THREADS = 256;
-constexpr int EXEC_WARPS = EXEC_THREADS / 32;
+// executor CTA (one per SM): 16 consumer warps + 2 producer warps (one per
+// task slot)
+constexpr int EXEC_CONSUMERS = 512;
+constexpr int EXEC_PRODUCERS = 2;
+constexpr int EXEC_THREADS = EXEC_CONSUMERS + 32 * EXEC_PRODUCERS;
+constexpr int EXEC_WARPS = EXEC_CONSUMERS / 32;
+constexpr int EXEC_MAX_STAGES = 8;  // operator piece ring (TMA bulk copies); the
+                                    // handle picks 2..8 stages from its smem budget
+constexpr int EXEC_TSLOTS = EXEC_PRODUCERS;  // task slots (metadata blob, staged vectors)
+constexpr int EXEC_EPI = 16;        // epilogue rows per task slot (>= PLR_TILE, DENSE_RT_MAX)
+constexpr int EXEC_EPI_SRC = 6;     // epilogue source rows: init, eyes (<= 4), rhs
+constexpr int EXEC_TERMS = 16;      // term scales per task slot
+constexpr int EXEC_EYES = EXEC_EPI_SRC - 2;
+constexpr int EXEC_TRACE = 24;      // u64 trace words per task (pt_trace_program)
+constexpr int EXEC_PIECES = 48;     // operator pieces of one task (descriptors in the slot)
+constexpr int EXEC_SRCS = 2 * EXEC_TERMS + EXEC_EPI_SRC;  // vector pointers of one task
+constexpr int EXEC_WAITS = 16;      // dependency counters of one task
+constexpr int EXEC_RUNS = 256;      // t-value runs of one Y_PLR task
 constexpr int DENSE_RT_MAX = 4;   // max rows of a Y_DENSE task (split-K over warps)
 constexpr int DENSE_ROWS_PER_TASK = 4;
 
@@ -83,8 +99,16 @@ struct ExecArgs {
   const DevTileEntry* tile_ent;
   const DevTileEntry* ents;  // program's Y_PLR task entries
   const DevPiece* pieces;    // program's staged operator ranges
-  int64_t half_elems;        // complex capacity of one smem buffer half
-  int64_t src_cap;           // complex capacity of the source / t staging area
+  const DevItem* items;      // program's per-column / per-slot task metadata
+  // per-task metadata blobs in queue order (see pt_api.cu build_blobs): task q
+  // is blob[blob_off[q] .. blob_off[q+1]) in 16-byte units
+  const int4* blob;
+  const int64_t* blob_off;
+  int64_t half_elems;        // complex capacity of one ring stage
+  int64_t src_cap;           // complex capacity of a task slot's vector staging area
+  int64_t blob_cap;          // bytes of a task slot's blob area
+  int64_t slot_bytes;        // bytes of one task slot
+  int32_t n_stages;          // ring stages (<= EXEC_MAX_STAGES)
   const int* stop;  // GMRES status stop flag: the whole launch is skipped once set
   // iteration-relative basis addressing (GMRES loop inside a graph):
   // if iter != nullptr, SLOT_IN = vbase + (*iter) * vstride, SLOT_OUT = SLOT_IN + vstride

@@ -1,283 +1,553 @@
 // Persistent dataflow executor for interface-operator programs.
 //
-// One launch runs a whole program (an A-apply, a preconditioner apply of
-// n_it Gauss-Seidel sweeps, or a fused A -> M GMRES iteration).  CTAs pull
-// task indices from a global queue in priority order (topological: every
-// dependency of task q sits at an index < q), wait on the counters of the
-// producer groups they read, compute, and bump their own group's counter.
-// The launch is cooperative, so every CTA is resident and a CTA waiting on a
-// counter always has a running producer: no deadlock, no grid barrier, and
-// the sequential sweep chain overlaps the independent A-apply / R-term work.
+// One launch runs a whole program: an A-apply, a preconditioner apply of
+// n_it Gauss-Seidel sweeps, or a fused A -> M GMRES iteration.  The host
+// compiles the program into a task DAG whose queue order is topological.
+// Tasks wait on the counters of the producer groups they read and bump
+// their own group's counter.  The launch is cooperative: every CTA is
+// resident, so a waiting task always has a running producer.
 //
-// Operator data moves HBM -> shared memory with TMA bulk copies
-// (cp.async.bulk.shared::cluster.global, completion on an mbarrier).  Every
-// task's operator bytes are a few contiguous "pieces" (host layout: a Vt
-// region per kernel and tile-major U chunks), double-buffered in two smem
-// halves.  The first two pieces are issued when the task is grabbed, BEFORE
-// its dependency wait: the operator never depends on the iterate, so a sweep
-// level's kernels stream in while the previous level is still computing.
-// After the wait the task stages its (small) vector inputs, waits for the
-// pieces and computes from shared memory (FP64 FMA, fixed-order sums, no
-// float atomics: repeated applies are bitwise identical).
+// Each CTA is warp-specialised.  Two producer warps own one task slot each
+// and take the CTA's tasks alternately (grabbed one at a time, in order);
+// per task a producer warp:
+//   - bulk-copies the task's metadata blob (descriptor, operator pieces,
+//     terms, eyes, waits, per-column items) into its slot: one TMA copy;
+//   - issues the task's operator pieces into the CTA's smem ring with TMA
+//     bulk copies (cp.async.bulk, mbarrier complete_tx) as far as the ring
+//     allows -- BEFORE the dependency wait, when it is this task's turn;
+//   - waits for the dependency counters;
+//   - gathers the vector inputs (source slice, t values, term sources,
+//     epilogue rows) with cp.async, all copies in flight at once;
+//   - hands the slot to the consumers (mbarrier), then streams the task's
+//     remaining pieces and passes the ring to the next task.
+// With two producer warps the metadata, dependency and staging latency of
+// task n+1 overlaps the consumers' work on task n, and the operator stream
+// of the next sweep level overlaps the current level's dependency chain.
+// The 8 consumer warps compute from shared memory (FP64 FMA, fixed-order
+// sums), release ring stages and slots through mbarriers, write the outputs
+// and signal the counters.  No float atomics anywhere: every output element
+// is produced by one CTA in a fixed order, so repeated applies are bitwise
+// identical.
 #include "pt_device.cuh"
 
 namespace pt {
 
 namespace {
 
-// slot base pointers of this launch (iteration-relative ones resolved)
-__shared__ double2* s_slot[N_SLOTS];
-__shared__ __align__(8) unsigned long long s_bar[2];  // one mbarrier per buffer half
+constexpr int CONSUMERS = EXEC_CONSUMERS;  // 512 threads, 16 warps
+constexpr int CWARPS = CONSUMERS / 32;
 
-__device__ __forceinline__ const double2* vptr(const VecRef& r) { return s_slot[r.slot] + r.off; }
-__device__ __forceinline__ double2* vptr_w(const VecRef& r) { return s_slot[r.slot] + r.off; }
+__shared__ double2* s_slot[N_SLOTS];
+__shared__ __align__(8) unsigned long long s_full[EXEC_MAX_STAGES];   // piece landed (tx)
+__shared__ __align__(8) unsigned long long s_empty[EXEC_MAX_STAGES];  // piece consumed
+__shared__ __align__(8) unsigned long long s_tfull[EXEC_TSLOTS];      // slot handed over
+__shared__ __align__(8) unsigned long long s_tempty[EXEC_TSLOTS];     // slot released
+__shared__ __align__(8) unsigned long long s_meta[EXEC_TSLOTS];       // blob landed (tx)
+__shared__ __align__(8) unsigned long long s_stg[EXEC_TSLOTS];        // vectors landed (tx)
+__shared__ volatile int s_grab_turn;     // slot use whose task may be grabbed next
+__shared__ volatile int s_issue_turn;    // slot use whose pieces may be issued
+__shared__ volatile uint32_t s_seq;      // operator pieces issued so far (ring position)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-
-// thread 0: stage one piece into a buffer half (TMA bulk copy, mbarrier tx)
-__device__ __forceinline__ void issue_piece(unsigned long long* bar, double2* dst,
-                                            const double2* src, uint32_t bytes) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+__device__ __forceinline__ void bar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
                "r"(bytes)
                : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
-
-__device__ __forceinline__ void wait_bar(unsigned long long* bar, uint32_t phase) {
+__device__ __forceinline__ bool bar_test(unsigned long long* b, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(done)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* b, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
+        : "r"(smem_u32(b)), "r"(parity)
         : "memory");
   }
 }
+// TMA bulk copy global -> this CTA's shared memory, completing on mbarrier b
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes,
+                                          unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS) : "memory");
+}
+// 16-byte asynchronous global -> shared copy through L2 (vectors written by
+// other CTAs inside the launch: L1 is bypassed)
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-struct Smem {
-  double2* half[2];    // operator piece buffers
-  double2* src;        // staged source vector (m) / t values (MAX_TCOLS)
-  double2* part;       // EXEC_THREADS partial sums
-  void* meta;          // task metadata (entries / slots)
+// ---- shared-memory layout -------------------------------------------------------
+
+// A task slot: [metadata blob][staged vectors][epilogue rows][coefficients]
+// [vector pointers].  Blob sections are located by the descriptor's offsets.
+struct Slot {
+  char* blob;
+  double2* vec;         // staged vector inputs (source slice / t values / term sources)
+  double2* epi;         // epilogue source rows: [k * EXEC_EPI + row], k = init, eyes, rhs
+  double2* coef;        // term scales [0, EXEC_TERMS), eye coefficients after them
+  const double2** src;  // vector pointers: term sources [2 * term + s], then
+                        // epilogue rows [2 * EXEC_TERMS + k]
+  __device__ __forceinline__ const DevTask& desc() const {
+    return *reinterpret_cast<const DevTask*>(blob);
+  }
+  __device__ __forceinline__ const DevPiece* pieces() const {
+    return reinterpret_cast<const DevPiece*>(blob + desc().piece0);
+  }
+  __device__ __forceinline__ const DevTerm* terms() const {
+    return reinterpret_cast<const DevTerm*>(blob + desc().term0);
+  }
+  __device__ __forceinline__ const DevEye* eyes() const {
+    return reinterpret_cast<const DevEye*>(blob + desc().eye0);
+  }
+  __device__ __forceinline__ const DevWait* waits() const {
+    return reinterpret_cast<const DevWait*>(blob + desc().wait0);
+  }
+  __device__ __forceinline__ const DevItem* items() const {
+    return reinterpret_cast<const DevItem*>(blob + desc().item0);
+  }
+  __device__ __forceinline__ const DevRun* runs() const {
+    return reinterpret_cast<const DevRun*>(blob + desc().run0);
+  }
 };
 
-__device__ __forceinline__ Smem carve(double2* base, const ExecArgs& a) {
-  Smem s;
-  s.half[0] = base;
-  s.half[1] = base + a.half_elems;
-  s.src = base + 2 * a.half_elems;
-  s.part = s.src + a.src_cap;
-  s.meta = s.part + EXEC_THREADS;
-  return s;
-}
-
-// per-CTA pipeline state (uniform across threads)
-struct Pipe {
-  uint32_t phase[2];
+// computed on use (arrays of pointers would be indexed dynamically and live
+// on the stack)
+struct Layout {
+  char* base;
+  int64_t stage_bytes, slot_bytes, blob_cap, vec_cap;
+  int n_stages;
+  __device__ __forceinline__ double2* stage(int s) const {
+    return reinterpret_cast<double2*>(base + (size_t)s * stage_bytes);
+  }
+  __device__ __forceinline__ Slot slot(int k) const {
+    char* q = base + (size_t)n_stages * stage_bytes + (size_t)k * slot_bytes;
+    Slot sl;
+    sl.blob = q;
+    q += blob_cap;
+    sl.vec = reinterpret_cast<double2*>(q);
+    q += (size_t)vec_cap * sizeof(double2);
+    sl.epi = reinterpret_cast<double2*>(q);
+    q += EXEC_EPI * EXEC_EPI_SRC * sizeof(double2);
+    sl.coef = reinterpret_cast<double2*>(q);
+    q += (EXEC_TERMS + EXEC_EYES) * sizeof(double2);
+    sl.src = reinterpret_cast<const double2**>(q);
+    return sl;
+  }
+  __device__ __forceinline__ double2* part() const {
+    return reinterpret_cast<double2*>(base + (size_t)n_stages * stage_bytes +
+                                      EXEC_TSLOTS * (size_t)slot_bytes);
+  }
 };
 
-__device__ __forceinline__ const double2* pool_of(const ExecArgs& a, const DevTask& t) {
-  return t.type == TASK_Y_DENSE ? a.dense : a.fac;
+__device__ __forceinline__ Layout carve(double2* base, const ExecArgs& a) {
+  Layout L;
+  L.base = reinterpret_cast<char*>(base);
+  L.stage_bytes = a.half_elems * (int64_t)sizeof(double2);
+  L.slot_bytes = a.slot_bytes;
+  L.blob_cap = a.blob_cap;
+  L.vec_cap = a.src_cap;
+  L.n_stages = a.n_stages;
+  return L;
 }
 
-// thread 0 issues piece p of task t into half p % 2
-__device__ __forceinline__ void issue(const ExecArgs& a, const DevTask& t, const Smem& sm, int p) {
-  const DevPiece pc = a.pieces[t.piece0 + p];
-  issue_piece(&s_bar[p & 1], sm.half[p & 1], pool_of(a, t) + pc.src,
-              (uint32_t)pc.elems * (uint32_t)sizeof(double2));
+__device__ __forceinline__ const double2* vptr(const VecRef& r) { return s_slot[r.slot] + r.off; }
+__device__ __forceinline__ double2* vptr_w(const VecRef& r) { return s_slot[r.slot] + r.off; }
+
+// trace words of queue index q: 0 grab, 1 ready, 2 done, 3 smid | cta << 16,
+// 4 consumer start, 5 staged, 6..13 piece p landed (consumer), 14..21 piece p
+// issued (producer), 22/23 consumer cycles waiting for pieces / in barriers
+__device__ __forceinline__ void trace_mark(const ExecArgs& a, int q, int k) {
+  if (a.trace)
+    a.trace[EXEC_TRACE * (size_t)q + k] =
+        k == 3 ? (unsigned long long)smid() | ((unsigned long long)blockIdx.x << 16) : globaltimer();
 }
 
-__device__ __forceinline__ const double2* wait_piece(Pipe& pp, int p, const Smem& sm) {
-  wait_bar(&s_bar[p & 1], pp.phase[p & 1]);
-  pp.phase[p & 1] ^= 1u;
-  return sm.half[p & 1];
+// ---- producers (warps 8, 9) ---------------------------------------------------------
+
+// lane 0 of the warp holding the issue turn: piece p of the slot's task into
+// the ring stage of sequence number seq
+__device__ __forceinline__ void issue_piece(const ExecArgs& a, const Layout& L, const Slot& sl,
+                                            int q, int p, uint32_t seq) {
+  const DevPiece& pc = sl.pieces()[p];
+  const int s = seq % (uint32_t)L.n_stages;
+  const uint32_t bytes = (uint32_t)pc.elems * (uint32_t)sizeof(double2);
+  const double2* src = (sl.desc().type == TASK_Y_DENSE ? a.dense : a.fac) + pc.src;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  bar_expect(&s_full[s], bytes);
+  bulk_copy(L.stage(s), src, bytes, &s_full[s]);
+  if (p < 8) trace_mark(a, q, 14 + p);
 }
 
-// stage x_a [+ x_b] (length m) into smem
-__device__ __forceinline__ void stage_source(const DevTerm& tm, double2* s, int m) {
-  const double2* s0 = vptr(tm.src[0]);
-  if (tm.nsrc > 1) {
-    const double2* s1 = vptr(tm.src[1]);
-    for (int c = threadIdx.x; c < m; c += EXEC_THREADS) s[c] = cadd(ld_cg(s0 + c), ld_cg(s1 + c));
+// lane 0: is the ring stage of sequence number seq free for its next use?
+__device__ __forceinline__ bool stage_free(const Layout& L, uint32_t seq) {
+  const uint32_t ns = (uint32_t)L.n_stages;
+  return seq < ns || bar_test(&s_empty[seq % ns], ((seq / ns) - 1) & 1);
+}
+
+// Term scales, eye coefficients and the vector pointers the staging
+// dereferences, from the blob (all lanes; no global memory).
+__device__ __forceinline__ void parse_meta(const DevTask& t, const Slot& sl, int lane) {
+  if (lane < t.nterm) {
+    const DevTerm& tm = sl.terms()[lane];
+    sl.coef[lane] = make_double2(tm.scale_re, tm.scale_im);
+    sl.src[2 * lane] = vptr(tm.src[0]);
+    sl.src[2 * lane + 1] = tm.nsrc > 1 ? vptr(tm.src[1]) : nullptr;
+  }
+  const int e0 = t.has_init ? 1 : 0;
+  if (lane < t.neye) {
+    const DevEye& ey = sl.eyes()[lane];
+    sl.coef[EXEC_TERMS + lane] = make_double2(ey.re, ey.im);
+    sl.src[2 * EXEC_TERMS + e0 + lane] = vptr(ey.src);
+  }
+  if (lane == 0) {
+    if (t.has_init) sl.src[2 * EXEC_TERMS] = vptr(t.init);
+    if (t.has_rhs) sl.src[2 * EXEC_TERMS + e0 + t.neye] = vptr(t.rhs);
+  }
+}
+
+// The vector inputs of task t, after its dependencies (all 32 lanes): TMA
+// bulk copies of contiguous ranges (source slices, t-value runs, epilogue
+// rows) completing on the slot's staging barrier, all in flight at once.  A
+// merged term's second source lands right after the first and is added in
+// place (x_a + x_b, as the reference sums before applying the kernel).
+__device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& t, const Slot& sl,
+                                              int k, int& n_staged, int lane) {
+  const int nrows = t.r1 - t.r0;
+  const int nk = t.type == TASK_T_PLR ? 0 : (t.has_init ? 1 : 0) + t.neye + (t.has_rhs ? 1 : 0);
+  const int m = a.m;
+  uint32_t bytes = 0;  // total, for the barrier's transaction count
+  if (t.type == TASK_T_PLR) {
+    bytes = (uint32_t)(t.c1 - t.c0) * (sl.src[1] ? 2u : 1u);
+  } else if (t.type == TASK_Y_PLR) {
+    bytes = (uint32_t)t.nitem;
   } else {
-    for (int c = threadIdx.x; c < m; c += EXEC_THREADS) s[c] = ld_cg(s0 + c);
+    for (int it = 0; it < t.nterm; ++it) bytes += (uint32_t)m * (sl.src[2 * it + 1] ? 2u : 1u);
+  }
+  bytes = (bytes + (uint32_t)(nk * nrows)) * (uint32_t)sizeof(double2);
+  if (bytes == 0) return;
+  const uint32_t phase = (uint32_t)(n_staged++ & 1);
+  if (lane == 0) {
+    // sources written by other CTAs (generic proxy) are read by the TMA
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_stg[k])),
+                 "r"(bytes)
+                 : "memory");
+  }
+  __syncwarp();
+  if (t.type == TASK_T_PLR) {
+    const uint32_t nb = (uint32_t)(t.c1 - t.c0) * (uint32_t)sizeof(double2);
+    if (lane == 0) bulk_copy(sl.vec, sl.src[0] + t.c0, nb, &s_stg[k]);
+    if (lane == 1 && sl.src[1]) bulk_copy(sl.vec + (t.c1 - t.c0), sl.src[1] + t.c0, nb, &s_stg[k]);
+  } else if (t.type == TASK_Y_PLR) {
+    const double2* T = s_slot[SLOT_T];
+    const DevRun* runs = sl.runs();
+    for (int i = lane; i < t.nrun; i += 32) {
+      const DevRun r = runs[i];
+      bulk_copy(sl.vec + r.f, T + r.t, (uint32_t)r.n * (uint32_t)sizeof(double2), &s_stg[k]);
+    }
+  } else {
+    for (int i = lane; i < 2 * t.nterm; i += 32)
+      if (const double2* src = sl.src[i])
+        bulk_copy(sl.vec + i * m, src, (uint32_t)m * (uint32_t)sizeof(double2), &s_stg[k]);
+  }
+  if (lane < nk)  // epilogue source rows: init, eyes, rhs
+    bulk_copy(sl.epi + lane * EXEC_EPI, sl.src[2 * EXEC_TERMS + lane] + t.r0,
+              (uint32_t)nrows * (uint32_t)sizeof(double2), &s_stg[k]);
+  __syncwarp();
+  if (lane == 0) bar_arrive(&s_stg[k]);
+  bar_wait(&s_stg[k], phase);
+  if (t.type == TASK_T_PLR) {
+    if (sl.src[1]) {
+      const int n = t.c1 - t.c0;
+      for (int c = lane; c < n; c += 32) sl.vec[c] = cadd(sl.vec[c], sl.vec[n + c]);
+    }
+  } else if (t.type == TASK_Y_DENSE) {
+    for (int it = 0; it < t.nterm; ++it)
+      if (sl.src[2 * it + 1])
+        for (int c = lane; c < m; c += 32)
+          sl.vec[2 * it * m + c] = cadd(sl.vec[2 * it * m + c], sl.vec[(2 * it + 1) * m + c]);
   }
 }
 
-// final per-row epilogue: init + partial sum + eyes + rhs -> out
-__device__ __forceinline__ void finish_row(const ExecArgs& a, const DevTask& t, int row,
-                                           double2 v) {
-  if (t.has_init) v = cadd(ld_cg(vptr(t.init) + row), v);
-  for (int e = 0; e < t.neye; ++e) {
-    const DevEye ey = a.eyes[t.eye0 + e];
-    v = cfma(make_double2(ey.re, ey.im), ld_cg(vptr(ey.src) + row), v);
+// Producer warp k: slot k, the CTA's slot uses i = k, k + 2, k + 4, ...
+__device__ void producer(const ExecArgs& a, const Layout& L, int k) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ns = (uint32_t)L.n_stages;
+  const Slot sl = L.slot(k);
+  int n_staged = 0;  // phases of this slot's staging barrier
+  for (int j = 0;; ++j) {
+    const int use = 2 * j + k;
+    if (j > 0) {  // consumers done with use - 2: publish its outputs
+      bar_wait(&s_tempty[k], (j - 1) & 1);
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(a.ctr + sl.desc().signal, 1);
+      }
+    }
+    // one task per use, grabbed in use order (the CTA's uses run in
+    // increasing queue order, which the dependency argument needs)
+    int q = 0;
+    if (lane == 0) {
+      while (s_grab_turn != use) __nanosleep(16);
+      q = atomicAdd(a.head, 1);
+      s_grab_turn = use + 1;
+    }
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= a.n_tasks) {  // end: consumers stop at the first empty slot use
+      if (lane == 0) {
+        reinterpret_cast<DevTask*>(sl.blob)->type = -1;
+        bar_arrive(&s_tfull[k]);
+      }
+      return;
+    }
+    // the task's metadata blob: one bulk copy
+    if (lane == 0) {
+      trace_mark(a, q, 0);
+      const int64_t o0 = __ldg(a.blob_off + q), o1 = __ldg(a.blob_off + q + 1);
+      const uint32_t bytes = (uint32_t)((o1 - o0) * 16);
+      bar_expect(&s_meta[k], bytes);
+      bulk_copy(sl.blob, a.blob + o0, bytes, &s_meta[k]);
+    }
+    bar_wait(&s_meta[k], j & 1);
+    const DevTask& t = sl.desc();
+    parse_meta(t, sl, lane);
+    int issued = 0;
+    if (lane == 0) {
+      if (s_issue_turn == use) {  // our turn on the ring: pieces before the wait
+        __threadfence_block();
+        uint32_t seq = s_seq;
+        while (issued < t.npiece && stage_free(L, seq)) issue_piece(a, L, sl, q, issued++, seq++);
+        s_seq = seq;
+      }
+      const DevWait* w = sl.waits();
+      for (int i = 0; i < t.nwait; ++i)  // dependencies
+        while (ld_acquire(a.ctr + w[i].ctr) < w[i].val) __nanosleep(20);
+      trace_mark(a, q, 1);
+    }
+    __syncwarp();
+    stage_vectors(a, t, sl, k, n_staged, lane);
+    __syncwarp();
+    if (lane == 0) {
+      trace_mark(a, q, 5);
+      bar_arrive(&s_tfull[k]);  // release: blob, vectors, epilogue visible to consumers
+      // the rest of the task's pieces, in ring order after the previous use's
+      while (s_issue_turn != use) __nanosleep(32);
+      __threadfence_block();
+      uint32_t seq = s_seq;
+      while (issued < t.npiece) {
+        if (seq >= ns) bar_wait(&s_empty[seq % ns], ((seq / ns) - 1) & 1);
+        issue_piece(a, L, sl, q, issued++, seq++);
+      }
+      s_seq = seq;
+      __threadfence_block();
+      s_issue_turn = use + 1;
+    }
+    __syncwarp();
   }
+}
+
+// ---- consumers (warps 0-7) ---------------------------------------------------------
+
+// profiling (trace only): consumer thread 0's cycles waiting for pieces and
+// in the per-piece barrier, per task
+__shared__ long long s_cyc_wait, s_cyc_sync;
+
+__device__ __forceinline__ const double2* wait_piece(const ExecArgs& a, const Layout& L,
+                                                     uint32_t seq, int q, int p) {
+  const uint32_t ns = (uint32_t)L.n_stages;
+  const int s = seq % ns;
+  const long long c0 = a.trace ? clock64() : 0;
+  bar_wait(&s_full[s], (seq / ns) & 1);
+  if (a.trace && threadIdx.x == 0) {
+    s_cyc_wait += clock64() - c0;
+    if (p < 8) trace_mark(a, q, 6 + p);
+  }
+  return L.stage(s);
+}
+
+__device__ __forceinline__ void release_piece(const ExecArgs& a, const Layout& L, uint32_t& seq) {
+  const long long c0 = a.trace ? clock64() : 0;
+  consumer_sync();
+  if (threadIdx.x == 0) {
+    if (a.trace) s_cyc_sync += clock64() - c0;
+    bar_arrive(&s_empty[seq % (uint32_t)L.n_stages]);
+  }
+  ++seq;
+}
+
+// T_PLR: t = scale * Vt (x_a [+ x_b]).  A group of L lanes (L = 8, 16 or 32
+// per piece, from the widest row) per Vt row: lane j sums columns j, j + L,
+// ... in order, then an xor tree over the group.
+__device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, const Slot& sl,
+                                          const Layout& L, uint32_t& seq, int q) {
+  double2* T = s_slot[SLOT_T];
+  const double2 sc = sl.coef[0];
+  const DevItem* items = sl.items();
+  for (int p = 0; p < t.npiece; ++p) {
+    const DevPiece& pc = sl.pieces()[p];
+    const int lanes = pc.e0;
+    const int sub = threadIdx.x & (lanes - 1);
+    const double2* buf = wait_piece(a, L, seq, q, p);
+    for (int base = pc.f0; base < pc.f1; base += CONSUMERS / lanes) {
+      const int r = base + (int)threadIdx.x / lanes;
+      double2 acc = make_double2(0.0, 0.0);
+      DevItem it{};
+      if (r < pc.f1) {
+        it = items[r];
+        const double2* V = buf + it.poff;
+        const double2* x = sl.vec + it.lo;
+        for (int c = sub; c < it.n; c += lanes) acc = cfma(V[c], x[c], acc);
+      }
+      for (int o = lanes >> 1; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (r < pc.f1 && sub == 0) st_cg(T + t.tbase + r, cmul(sc, acc));
+    }
+    release_piece(a, L, seq);
+  }
+}
+
+// init + eyes + rhs of one output row (fixed order), from the staged rows
+__device__ __forceinline__ double2 epilogue_row(const DevTask& t, const Slot& sl, int row) {
+  double2 v = make_double2(0.0, 0.0);
+  int k = 0;
+  if (t.has_init) v = sl.epi[k++ * EXEC_EPI + row];
+  for (int e = 0; e < t.neye; ++e, ++k) v = cfma(sl.coef[EXEC_TERMS + e], sl.epi[k * EXEC_EPI + row], v);
   if (t.has_rhs) {
-    const double2 r = ld_cg(vptr(t.rhs) + row);
+    const double2 r = sl.epi[k * EXEC_EPI + row];
     v.x = fma(t.rhs_coef, r.x, v.x);
     v.y = fma(t.rhs_coef, r.y, v.y);
   }
-  st_cg(vptr_w(t.out) + row, v);
+  return v;
 }
 
-// ---- metadata staging (before the dependency wait) --------------------------------
-
-__device__ __forceinline__ void stage_meta(const ExecArgs& a, const DevTask& t, const Smem& sm) {
-  if (t.type == TASK_Y_PLR) {
-    DevTileEntry* ent = reinterpret_cast<DevTileEntry*>(sm.meta);
-    for (int i = threadIdx.x; i < t.nent; i += EXEC_THREADS) ent[i] = a.ents[t.ent0 + i];
-  } else if (t.type == TASK_T_PLR) {
-    const DevTerm tm = a.terms[t.term0];
-    const int32_t slot0 = a.kplr[tm.kernel].slot0;
-    DevSlot* sl = reinterpret_cast<DevSlot*>(sm.meta);
-    for (int q = threadIdx.x; q < t.r1 - t.r0; q += EXEC_THREADS) sl[q] = a.slots[slot0 + t.r0 + q];
+// Y_PLR: one PLR_TILE-row tile; thread = (row r, column group g); columns
+// f = g (mod 16) ascending; the 16 group sums per row added in group order.
+__device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, const Slot& sl,
+                                          const Layout& L, uint32_t& seq, int q) {
+  constexpr int G = CONSUMERS / PLR_TILE;
+  const int r = threadIdx.x % PLR_TILE, g = threadIdx.x / PLR_TILE;
+  const DevItem* items = sl.items();
+  double2 acc = make_double2(0.0, 0.0);
+  for (int p = 0; p < t.npiece; ++p) {
+    const DevPiece& pc = sl.pieces()[p];
+    const double2* buf = wait_piece(a, L, seq, q, p);
+    for (int f = pc.f0 + ((g - pc.f0) % G + G) % G; f < pc.f1; f += G) {
+      const DevItem it = items[f];
+      if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
+    }
+    release_piece(a, L, seq);
+  }
+  double2* part = L.part();
+  part[g * PLR_TILE + r] = acc;
+  consumer_sync();
+  if ((int)threadIdx.x < t.r1 - t.r0) {
+    double2 v = epilogue_row(t, sl, threadIdx.x);
+#pragma unroll
+    for (int i = 0; i < G; ++i) v = cadd(v, part[i * PLR_TILE + threadIdx.x]);
+    st_cg(vptr_w(t.out) + t.r0 + threadIdx.x, v);
   }
 }
 
-// ---- Y_DENSE: rows [r0, r1) from dense kernel terms -------------------------------
-// piece p = rows r0..r1 of term p's kernel (row-major, staged in smem).
-// Columns are split over the 8 warps; each warp keeps its scaled partial per
-// row in smem; partials are added in warp order.
-__device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t, const Smem& sm, Pipe& pp) {
+// Y_DENSE: rows [r0, r1) (<= 4); piece p = rows of term p's kernel; columns
+// split over the 8 warps, per-warp scaled partials summed in warp order.
+__device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t, const Slot& sl,
+                                            const Layout& L, uint32_t& seq, int q) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.m;
   const int nrows = t.r1 - t.r0;
-  double2* part = sm.part;  // [EXEC_WARPS][DENSE_RT_MAX]
+  double2* part = L.part();
   if (lane < DENSE_RT_MAX) part[warp * DENSE_RT_MAX + lane] = make_double2(0.0, 0.0);
-  __syncthreads();  // partials visible to the final sum even when there are no terms
   for (int it = 0; it < t.nterm; ++it) {
-    const DevTerm tm = a.terms[t.term0 + it];
-    stage_source(tm, sm.src, m);
-    __syncthreads();
-    const double2* K = wait_piece(pp, it, sm);
+    const double2* K = wait_piece(a, L, seq, q, it);
+    const double2* x = sl.vec + 2 * it * m;
     double2 d[DENSE_RT_MAX];
 #pragma unroll
-    for (int k = 0; k < DENSE_RT_MAX; ++k) d[k] = make_double2(0.0, 0.0);
-    for (int c = 32 * warp + lane; c < m; c += EXEC_THREADS) {
-      const double2 sv = sm.src[c];
+    for (int i = 0; i < DENSE_RT_MAX; ++i) d[i] = make_double2(0.0, 0.0);
+    for (int c = 32 * warp + lane; c < m; c += CONSUMERS) {
+      const double2 sv = x[c];
 #pragma unroll
-      for (int k = 0; k < DENSE_RT_MAX; ++k)
-        if (k < nrows) d[k] = cfma(K[k * m + c], sv, d[k]);
+      for (int i = 0; i < DENSE_RT_MAX; ++i)
+        if (i < nrows) d[i] = cfma(K[i * m + c], sv, d[i]);
     }
-    const double2 sc = make_double2(tm.scale_re, tm.scale_im);
+    const double2 sc = sl.coef[it];
 #pragma unroll
-    for (int k = 0; k < DENSE_RT_MAX; ++k) {
-      const double2 r = warp_sum(d[k]);
-      if (lane == k && k < nrows)
-        part[warp * DENSE_RT_MAX + k] = cfma(sc, r, part[warp * DENSE_RT_MAX + k]);
+    for (int i = 0; i < DENSE_RT_MAX; ++i) {
+      const double2 rr = warp_sum(d[i]);
+      if (lane == i && i < nrows)
+        part[warp * DENSE_RT_MAX + i] = cfma(sc, rr, part[warp * DENSE_RT_MAX + i]);
     }
-    __syncthreads();  // buffer half and source free
-    if (threadIdx.x == 0 && it + 2 < t.npiece) issue(a, t, sm, it + 2);
+    release_piece(a, L, seq);
   }
-  if ((int)threadIdx.x >= nrows) return;
-  double2 v = make_double2(0.0, 0.0);
-  for (int w = 0; w < EXEC_WARPS; ++w) v = cadd(v, part[w * DENSE_RT_MAX + threadIdx.x]);
-  finish_row(a, t, t.r0 + threadIdx.x, v);
-}
-
-// ---- T_PLR: t = scale * Vt (x_a [+ x_b]) for a slot range ----------------------------
-// The Vt rows of the task are one piece (contiguous in the Vt region); warp per
-// Vt row, lanes across columns, everything from smem.  The term's scale is
-// folded into t so the Y phase is a plain U t sum.
-__device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, const Smem& sm, Pipe& pp) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const DevTerm tm = a.terms[t.term0];
-  double2* T = s_slot[SLOT_T] + tm.t_base;
-  stage_source(tm, sm.src, a.m);
-  __syncthreads();
-  const DevSlot* sl = reinterpret_cast<const DevSlot*>(sm.meta);
-  const double2 sc = make_double2(tm.scale_re, tm.scale_im);
-  for (int p = 0; p < t.npiece; ++p) {
-    const DevPiece pc = a.pieces[t.piece0 + p];
-    const double2* buf = wait_piece(pp, p, sm);
-    for (int q = pc.f0 + warp; q < pc.f1; q += EXEC_WARPS) {
-      const DevSlot d = sl[q];
-      const double2* V = buf + (d.v_off - pc.src);
-      const double2* x = sm.src + d.col_off;
-      double2 r = make_double2(0.0, 0.0);
-      for (int c = lane; c < d.cols; c += 32) r = cfma(V[c], x[c], r);
-      r = warp_sum(r);
-      if (lane == 0) st_cg(T + t.r0 + q, cmul(sc, r));
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && p + 2 < t.npiece) issue(a, t, sm, p + 2);
+  consumer_sync();
+  if ((int)threadIdx.x < nrows) {
+    double2 v = epilogue_row(t, sl, threadIdx.x);
+    for (int w = 0; w < CWARPS; ++w) v = cadd(v, part[w * DENSE_RT_MAX + threadIdx.x]);
+    st_cg(vptr_w(t.out) + t.r0 + threadIdx.x, v);
   }
 }
 
-// ---- Y_PLR: one PLR_TILE-row tile ---------------------------------------------------
-// y_r = sum over the task's flat (entry, rank column) list of U[r, c] t[c].
-// Thread = (row r = tid % 16, column group g = tid / 16): group g takes flat
-// columns f = g (mod 16) in ascending order; the 16 partial sums per row are
-// added in group order.  U pieces and the t values are read from smem.
-__device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, const Smem& sm, Pipe& pp) {
-  constexpr int G = EXEC_THREADS / PLR_TILE;  // 16 column groups
-  const int r = threadIdx.x % PLR_TILE, g = threadIdx.x / PLR_TILE;
-  const DevTileEntry* ent = reinterpret_cast<const DevTileEntry*>(sm.meta);
-  // t values of every flat column (produced by this level's T tasks)
-  double2* ts = sm.src;
-  {
-    const double2* T = s_slot[SLOT_T];
-    int e = 0;
-    for (int f = threadIdx.x; f < t.ncol; f += EXEC_THREADS) {
-      while (e + 1 < t.nent && f >= ent[e + 1].pre) ++e;
-      ts[f] = ld_cg(T + ent[e].t0 + (f - ent[e].pre));
-    }
-  }
-  __syncthreads();
-  double2 acc = make_double2(0.0, 0.0);
-  for (int p = 0; p < t.npiece; ++p) {
-    const DevPiece pc = a.pieces[t.piece0 + p];
-    const double2* buf = wait_piece(pp, p, sm);
-    int e = pc.e0;
-    // first column of this group inside the piece
-    int f = pc.f0 + ((g - pc.f0) % G + G) % G;
-    for (; f < pc.f1; f += G) {
-      while (e + 1 < t.nent && f >= ent[e + 1].pre) ++e;
-      const DevTileEntry en = ent[e];
-      if (r >= en.lo && r < en.hi) {
-        const int c = f - en.pre;
-        const double2 u = buf[en.u0 + (int64_t)c * en.stride - pc.src + (r - en.lo)];
-        acc = cfma(u, ts[f], acc);
+__device__ void consumer(const ExecArgs& a, const Layout& L) {
+  uint32_t seq = 0;  // pieces consumed
+  for (int use = 0;; ++use) {
+    const int k = use % EXEC_TSLOTS;
+    const Slot sl = L.slot(k);
+    bar_wait(&s_tfull[k], (use / EXEC_TSLOTS) & 1);  // acquire the producer's staging
+    const DevTask& t = sl.desc();
+    if (t.type < 0) return;
+    const int q = t.q;
+    if (threadIdx.x == 0) trace_mark(a, q, 4);
+    if (t.type == TASK_T_PLR)
+      run_t_plr(a, t, sl, L, seq, q);
+    else if (t.type == TASK_Y_PLR)
+      run_y_plr(a, t, sl, L, seq, q);
+    else
+      run_y_dense(a, t, sl, L, seq, q);
+    consumer_sync();
+    if (threadIdx.x == 0) {  // the slot's producer warp publishes the outputs
+      trace_mark(a, q, 2);
+      trace_mark(a, q, 3);
+      if (a.trace) {
+        a.trace[EXEC_TRACE * (size_t)q + 22] = s_cyc_wait;
+        a.trace[EXEC_TRACE * (size_t)q + 23] = s_cyc_sync;
+        s_cyc_wait = s_cyc_sync = 0;
       }
+      bar_arrive(&s_tempty[k]);
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && p + 2 < t.npiece) issue(a, t, sm, p + 2);
   }
-  sm.part[g * PLR_TILE + r] = acc;
-  __syncthreads();
-  if ((int)threadIdx.x >= PLR_TILE || t.r0 + (int)threadIdx.x >= t.r1) return;
-  double2 v = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int q = 0; q < G; ++q) v = cadd(v, sm.part[q * PLR_TILE + threadIdx.x]);
-  finish_row(a, t, t.r0 + threadIdx.x, v);
 }
 
 }  // namespace
 
-// thread 0: asynchronous copy of a task descriptor into smem (cp.async)
-__device__ __forceinline__ void fetch_task(DevTask* dst, const DevTask* src) {
-  static_assert(sizeof(DevTask) % 16 == 0, "DevTask must be a multiple of 16 bytes");
-  const char* s = reinterpret_cast<const char*>(src);
-  const uint32_t d = smem_u32(dst);
-#pragma unroll
-  for (int i = 0; i < (int)(sizeof(DevTask) / 16); ++i)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * i), "l"(s + 16 * i)
-                 : "memory");
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-__global__ void __launch_bounds__(EXEC_THREADS, 3) pt_exec_kernel(ExecArgs a) {
+__global__ void __launch_bounds__(EXEC_THREADS, 1) pt_exec_kernel(ExecArgs a) {
   extern __shared__ __align__(128) double2 smem[];
-  __shared__ __align__(16) DevTask s_desc[2];  // current / next task descriptors
-  __shared__ int s_q[2];
   __shared__ int s_stop;
   if (a.stop) {
     if (threadIdx.x == 0) s_stop = *((volatile const int*)a.stop);
@@ -293,65 +563,28 @@ __global__ void __launch_bounds__(EXEC_THREADS, 3) pt_exec_kernel(ExecArgs a) {
     s_slot[threadIdx.x] = p;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[i])) : "memory");
+    s_cyc_wait = s_cyc_sync = 0;
+    s_issue_turn = 0;
+    s_grab_turn = 0;
+    s_seq = 0;
+    for (int i = 0; i < a.n_stages; ++i) {
+      bar_init(&s_full[i], 1);
+      bar_init(&s_empty[i], 1);
+    }
+    for (int i = 0; i < EXEC_TSLOTS; ++i) {
+      bar_init(&s_tfull[i], 1);
+      bar_init(&s_tempty[i], 1);
+      bar_init(&s_meta[i], 1);
+      bar_init(&s_stg[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int q0 = atomicAdd(a.head, 1);
-    s_q[0] = q0;
-    if (q0 < a.n_tasks) fetch_task(&s_desc[0], a.tasks + q0);
-    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
-  const Smem sm = carve(smem, a);
-  Pipe pp;
-  pp.phase[0] = pp.phase[1] = 0;
-  int b = 0;
-  for (;;) {
-    const int q = s_q[b];
-    if (q >= a.n_tasks) break;
-    const DevTask& t = s_desc[b];
-    int q_next = 0;
-    unsigned long long t_grab = 0, t_ready = 0;
-    // grab the next task now; its index is needed only after the wait below
-    if (threadIdx.x == 0) {
-      q_next = atomicAdd(a.head, 1);
-      if (a.trace) t_grab = globaltimer();
-      // prepare: start the operator copies (input independent)
-      for (int p = 0; p < t.npiece && p < 2; ++p) issue(a, t, sm, p);
-    }
-    stage_meta(a, t, sm);
-    // wait for the producers of the inputs; then prefetch the next descriptor
-    if (threadIdx.x == 0) {
-      for (int w = 0; w < t.nwait; ++w) {
-        const DevWait dw = a.waits[t.wait0 + w];
-        while (ld_acquire(a.ctr + dw.ctr) < dw.val) __nanosleep(32);
-      }
-      if (a.trace) t_ready = globaltimer();
-      s_q[b ^ 1] = q_next;
-      if (q_next < a.n_tasks) fetch_task(&s_desc[b ^ 1], a.tasks + q_next);
-    }
-    __syncthreads();
-    if (t.type == TASK_Y_DENSE)
-      run_y_dense(a, t, sm, pp);
-    else if (t.type == TASK_T_PLR)
-      run_t_plr(a, t, sm, pp);
-    else
-      run_y_plr(a, t, sm, pp);
-    if (threadIdx.x == 0) asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(a.ctr + t.signal, 1);
-      if (a.trace) {
-        unsigned long long* tr = a.trace + 4 * (size_t)q;
-        tr[0] = t_grab;
-        tr[1] = t_ready;
-        tr[2] = globaltimer();
-        tr[3] = smid();
-      }
-    }
-    b ^= 1;
-  }
+  const Layout L = carve(smem, a);
+  if (threadIdx.x >= CONSUMERS)
+    producer(a, L, (threadIdx.x - CONSUMERS) >> 5);
+  else
+    consumer(a, L);
 }
 
 }  // namespace pt

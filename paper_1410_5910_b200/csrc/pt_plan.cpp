@@ -24,6 +24,7 @@
 #include "pt_plan.h"
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <map>
 #include <queue>
@@ -55,6 +56,9 @@ VecRef ref(int32_t slot, int64_t off) {
 class Builder {
  public:
   Builder(const Operator& op, const PlanParams& pp) : op_(op), pp_(pp) {}
+  // pieces per T_PLR task for the blocks emitted next (0: pp.t_pieces)
+  int t_pieces_now = 0;
+  const PlanParams& params() const { return pp_; }
 
   int emit_block(VecRef out, const std::vector<TermSpec>& terms,
                  const std::vector<EyeSpec>& eyes, bool has_init, VecRef init,
@@ -96,26 +100,71 @@ class Builder {
           tk.piece0 = (int32_t)prog_.pieces.size();
           int32_t s1 = s0;
           int64_t total = 0;
-          const int32_t cap = std::min(pp_.plr_slots_per_task, MAX_T_SLOTS);
-          for (int np = 0; np < pp_.t_pieces && s1 < ns && s1 - s0 < cap; ++np) {
+          const int32_t cap = (int32_t)std::min<int64_t>(pp_.plr_slots_per_task, pp_.item_cap);
+          int32_t span0 = INT32_MAX, span1 = INT32_MIN;
+          bool span_full = false;
+          const int tp = t_pieces_now > 0 ? t_pieces_now : pp_.t_pieces;
+          for (int np = 0; np < tp && s1 < ns && s1 - s0 < cap && !span_full; ++np) {
             DevPiece pc{};
             pc.src = op_.slots[kp.slot0 + s1].v_off;
             pc.f0 = s1 - s0;
             int64_t elems = 0;
             while (s1 < ns && s1 - s0 < cap) {
-              const int64_t c = op_.slots[kp.slot0 + s1].cols;
+              const DevSlot& sl = op_.slots[kp.slot0 + s1];
+              const int64_t c = sl.cols;
               if (s1 - s0 > pc.f0 && elems + c > pp_.half_elems) break;
+              // the staged source slice [c0, c1) of the task stays within tcols_cap
+              const int32_t lo = std::min(span0, sl.col_off);
+              const int32_t hi = std::max(span1, sl.col_off + sl.cols);
+              if (s1 > s0 && hi - lo > pp_.tcols_cap) {
+                span_full = true;
+                break;
+              }
+              span0 = lo;
+              span1 = hi;
               elems += c;
               ++s1;
             }
-            if (elems > pp_.half_elems) overflow_ = true;
+            if (s1 - s0 == pc.f0) break;  // nothing fits next to the staged slice
+            if (elems > pp_.half_elems) flag("a Vt row exceeds an operator stage");
             pc.elems = (int32_t)elems;
             pc.f1 = s1 - s0;
+            // lanes per Vt row in the consumers' dot products (8, 16 or 32)
+            int32_t widest = 0;
+            for (int32_t q = s0 + pc.f0; q < s1; ++q)
+              widest = std::max(widest, op_.slots[kp.slot0 + q].cols);
+            pc.e0 = widest <= 64 ? 8 : widest <= 128 ? 16 : 32;
             prog_.pieces.push_back(pc);
             total += elems;
           }
           tk.r1 = s1;
           tk.npiece = (int32_t)prog_.pieces.size() - tk.piece0;
+          tk.c0 = (int32_t)op_.m;
+          tk.c1 = 0;
+          for (int32_t q = s0; q < s1; ++q) {
+            const DevSlot& sl = op_.slots[kp.slot0 + q];
+            tk.c0 = std::min(tk.c0, sl.col_off);
+            tk.c1 = std::max(tk.c1, sl.col_off + sl.cols);
+          }
+          // one item per slot: Vt row offset within its piece, source offset
+          // within the staged slice, destination in SLOT_T
+          tk.item0 = (int32_t)prog_.items.size();
+          tk.tbase = (int32_t)(dt.t_base + s0);
+          for (int32_t p = 0; p < tk.npiece; ++p) {
+            const DevPiece& pc = prog_.pieces[tk.piece0 + p];
+            for (int32_t q = pc.f0; q < pc.f1; ++q) {
+              const DevSlot& sl = op_.slots[kp.slot0 + s0 + q];
+              DevItem it{};
+              it.poff = (uint16_t)(sl.v_off - pc.src);
+              it.lo = (uint16_t)(sl.col_off - tk.c0);
+              it.hi = 0;
+              it.n = (uint16_t)sl.cols;
+              prog_.items.push_back(it);
+            }
+          }
+          tk.nitem = (int32_t)prog_.items.size() - tk.item0;
+          if (tk.nitem > pp_.item_cap) flag("a T task has more slots than a task slot holds");
+          if (tk.c1 - tk.c0 > pp_.tcols_cap) flag("a Vt row is wider than a task slot stages");
           push_task(tk, twaits, g, 16.0 * (double)total);
           s0 = s1;
         }
@@ -142,19 +191,25 @@ class Builder {
     for (int64_t r0 = 0; r0 < m; r0 += rpt) {
       DevTask tk{};
       tk.piece0 = (int32_t)prog_.pieces.size();
-      if (plr) {  // flat tile entries of all terms, t0 absolute, prefix column counts
-        tk.ent0 = (int32_t)prog_.ents.size();
-        int32_t pre = 0;
+      if (plr) {  // one item per flat (leaf, rank column) of all terms, pieces of whole columns
+        tk.item0 = (int32_t)prog_.items.size();
+        tk.run0 = (int32_t)prog_.runs.size();
+        int32_t f = 0;
         for (size_t it = 0; it < terms.size(); ++it) {
           const DevTerm& dt = prog_.terms[term0 + it];
           const int32_t k0 = op_.kplr[dt.kernel].tile0 + (int32_t)(r0 / PLR_TILE);
-          // pieces: whole columns of this term's (contiguous) tile chunk
           DevPiece pc{};
           bool open = false;
           for (int32_t e = op_.tile_ptr[k0]; e < op_.tile_ptr[k0 + 1]; ++e) {
-            DevTileEntry te = op_.tile_ent[e];
-            const int32_t eidx = (int32_t)prog_.ents.size() - tk.ent0;
-            for (int32_t c = 0; c < te.rank; ++c) {
+            const DevTileEntry& te = op_.tile_ent[e];
+            if (te.rank > 0) {
+              DevRun run{};
+              run.t = (int32_t)(dt.t_base + te.t0);
+              run.f = (int16_t)f;
+              run.n = (int16_t)te.rank;
+              prog_.runs.push_back(run);
+            }
+            for (int32_t c = 0; c < te.rank; ++c, ++f) {
               const int64_t addr = te.u0 + (int64_t)c * te.stride;
               if (open && pc.elems + te.stride > pp_.half_elems) {
                 prog_.pieces.push_back(pc);
@@ -163,23 +218,25 @@ class Builder {
               if (!open) {
                 pc = DevPiece{};
                 pc.src = addr;
-                pc.f0 = pre + c;
-                pc.e0 = eidx;
+                pc.f0 = f;
                 open = true;
               }
+              DevItem item{};
+              item.poff = (uint16_t)pc.elems;
+              item.lo = (uint16_t)te.lo;
+              item.hi = (uint16_t)te.hi;
+              item.n = 0;
+              prog_.items.push_back(item);
               pc.elems += te.stride;
-              pc.f1 = pre + c + 1;
+              pc.f1 = f + 1;
             }
-            te.t0 = (int32_t)(te.t0 + dt.t_base);
-            te.pre = pre;
-            pre += te.rank;
-            prog_.ents.push_back(te);
           }
           if (open) prog_.pieces.push_back(pc);
         }
-        tk.nent = (int32_t)prog_.ents.size() - tk.ent0;
-        tk.ncol = pre;
-        if (tk.nent > MAX_TILE_ENTRIES || tk.ncol > MAX_TCOLS) overflow_ = true;
+        tk.nitem = (int32_t)prog_.items.size() - tk.item0;
+        tk.nrun = (int32_t)prog_.runs.size() - tk.run0;
+        tk.ncol = f;
+        if (tk.nitem > pp_.item_cap) flag("a PLR row tile has more rank columns than a task slot holds");
       } else {
         for (size_t it = 0; it < terms.size(); ++it) {
           DevPiece pc{};
@@ -187,11 +244,13 @@ class Builder {
           pc.elems = (int32_t)((std::min<int64_t>(m, r0 + rpt) - r0) * m);
           pc.f0 = (int32_t)it;
           pc.f1 = (int32_t)it + 1;
-          if (pc.elems > pp_.half_elems) overflow_ = true;
+          if (pc.elems > pp_.half_elems) flag("dense kernel rows exceed an operator stage");
           prog_.pieces.push_back(pc);
         }
       }
       tk.npiece = (int32_t)prog_.pieces.size() - tk.piece0;
+      tk.c0 = 0;
+      tk.c1 = (int32_t)m;
       tk.type = plr ? TASK_Y_PLR : TASK_Y_DENSE;
       tk.r0 = (int32_t)r0;
       tk.r1 = (int32_t)std::min<int64_t>(m, r0 + rpt);
@@ -211,7 +270,10 @@ class Builder {
     return g;
   }
 
-  bool overflow() const { return overflow_; }
+  bool overflow() const { return !overflow_.empty(); }
+  void flag(const char* why) {
+    if (overflow_.empty()) overflow_ = why;
+  }
   void begin_stage() { sweep_kernels_.clear(); }
   void end_stage() {
     for (int64_t k : sweep_kernels_) prog_.algo_bytes += op_.kernel_bytes[k];
@@ -286,6 +348,8 @@ class Builder {
     out.eyes = prog_.eyes;
     out.ents = prog_.ents;
     out.pieces = prog_.pieces;
+    out.items = prog_.items;
+    out.runs = prog_.runs;
     out.t_elems = prog_.t_elems;
     out.term_bytes = prog_.term_bytes;
     out.algo_bytes = prog_.algo_bytes;
@@ -356,7 +420,7 @@ class Builder {
   std::vector<int> task_group_;
   std::vector<double> task_cost_;
   std::set<int64_t> sweep_kernels_;
-  bool overflow_ = false;
+  std::string overflow_;  // why the program cannot run (empty: it can)
 };
 
 bool same_scale(const TermSpec& t, const HostEntry& e) {
@@ -495,7 +559,9 @@ void emit_sweep(Builder& b, const Operator& op, VecRef rhs, bool has_uold, VecRe
       }
     }
   }
-  // chain, level by level, both halves interleaved
+  // chain, level by level, both halves interleaved; small T tasks: a level's
+  // t-phase spreads over all CTAs (its latency is on the critical path)
+  b.t_pieces_now = b.params().t_pieces_chain;
   for (int lv = 0; lv <= max_level; ++lv) {
     for (int h = 0; h < 2; ++h) {
       for (int64_t q = 0; q < nt; ++q) {
@@ -516,6 +582,7 @@ void emit_sweep(Builder& b, const Operator& op, VecRef rhs, bool has_uold, VecRe
       }
     }
   }
+  b.t_pieces_now = 0;
   b.end_stage();
 }
 

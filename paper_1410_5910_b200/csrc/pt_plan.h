@@ -42,12 +42,14 @@ struct Program {
   std::vector<DevWait> waits;
   std::vector<DevTileEntry> ents;  // Y_PLR task entries (t0 absolute, pre = prefix)
   std::vector<DevPiece> pieces;    // staged operator ranges of every task
+  std::vector<DevItem> items;      // per-task metadata items
+  std::vector<DevRun> runs;        // Y_PLR t-value runs
   int n_counters = 0;
   int64_t t_elems = 0;      // size of SLOT_T needed
   int64_t term_bytes = 0;   // kernel bytes actually streamed by the terms
   int64_t algo_bytes = 0;   // distinct kernels per apply/sweep
   int64_t slot_elems[N_SLOTS] = {0};  // minimum size of each slot vector
-  bool overflow = false;    // a Y_PLR task exceeds MAX_TILE_ENTRIES (not runnable)
+  std::string overflow;     // non-empty: why a task exceeds the executor's staging (not runnable)
   std::string describe() const;
 };
 
@@ -59,13 +61,16 @@ std::string sweep_diagonal_error(const Operator& op);
 // Program kinds.
 struct PlanParams {
   int ctas = 444;                // executor CTAs (queue-order simulation)
-  int64_t half_elems = 1024;     // complex capacity of one smem buffer half
+  int64_t half_elems = 1024;     // complex capacity of one operator piece stage
   double task_us = 2.0;          // fixed cost per task in the simulation
   double cta_gbs = 25.0;         // streaming rate of one CTA in the simulation
   int dense_rows_per_task = 16;  // Y_DENSE rows per task
   int plr_rows_per_task = PLR_TILE;  // Y_PLR rows per task (lane per row)
   int plr_slots_per_task = 64;   // T_PLR slots per task (warp per slot)
-  int t_pieces = 2;              // buffer-half pieces per T_PLR task
+  int t_pieces = 2;              // ring-stage pieces per T_PLR task
+  int t_pieces_chain = 1;        // ... in the sweeps' dependency chain
+  int64_t item_cap = 1 << 20;    // metadata items a task slot holds
+  int64_t tcols_cap = MAX_TCOLS; // source columns a T_PLR task stages
 };
 
 Program build_apply_A(const Operator& op, const PlanParams& pp);

@@ -58,6 +58,17 @@ struct DevWait {
   int32_t val;
 };
 
+// One contiguous operator range a task stages into a ring stage with a TMA
+// bulk copy.  Y_PLR: whole rank columns [f0, f1) of the task's flat column
+// list.  T_PLR: slots [f0, f1) of the task, e0 = consumer lanes per Vt row.
+// Y_DENSE: rows r0..r1 of term f0's kernel.
+struct DevPiece {
+  int64_t src;     // element offset into the operator pool (dense or factors)
+  int32_t elems;
+  int32_t f0, f1;
+  int32_t e0;
+};
+
 struct DevTask {
   int32_t type;
   int32_t r0, r1;      // rows [r0,r1) of the block (Y) or slots (T)
@@ -71,21 +82,34 @@ struct DevTask {
   VecRef init;         // Y: partial sum to start from
   VecRef rhs;          // Y: + rhs_coef * rhs
   double rhs_coef;
-  int32_t ent0, nent;  // Y_PLR: flat tile entries of all terms (program ents array)
-  int32_t piece0, npiece;  // operator ranges staged into smem (program pieces array)
-  int32_t ncol;        // Y_PLR: flat columns of the task
-  int32_t pad2;        // 16-byte multiple (cp.async copies of the descriptor)
+  int32_t item0, nitem;    // per-column (Y_PLR) / per-slot (T_PLR) items
+  int32_t piece0, npiece;  // operator ranges staged into smem
+  int32_t run0, nrun;      // Y_PLR: runs of contiguous t values
+  int32_t ncol;            // Y_PLR: flat columns of the task
+  int32_t c0, c1;          // T_PLR: source columns [c0, c1) its Vt rows read
+  int32_t tbase;           // T_PLR: SLOT_T index of the task's first Vt row
+  int32_t q;               // queue index (set in the executor's metadata blob)
+  int32_t pad[3];
 };
 
-// One contiguous operator range a task stages into a smem buffer half with a
-// TMA bulk copy.  Y_PLR: whole rank columns [f0, f1) of the task's flat column
-// list, e0 = task-relative entry holding f0.  T_PLR: slots [f0, f1) of the
-// task.  Y_DENSE: rows r0..r1 of term f0's kernel.
-struct DevPiece {
-  int64_t src;     // element offset into the operator pool (dense or factors)
-  int32_t elems;
-  int32_t f0, f1;
-  int32_t e0;
+// Per-task metadata item, 8 bytes, precomputed on the host.
+//  Y_PLR column: U data at its piece + poff, tile rows [lo, hi).
+//  T_PLR Vt row: data at its piece + poff, n columns, source at staged-slice
+//                offset lo; result to SLOT_T[tbase + row].
+struct DevItem {
+  uint16_t poff;
+  uint16_t lo;
+  uint16_t hi;
+  uint16_t n;
+};
+static_assert(sizeof(DevItem) == 8, "DevItem is 8 bytes");
+static_assert(sizeof(DevTask) % 16 == 0, "DevTask is copied in 16-byte words");
+
+// Y_PLR: the t values of flat columns [f, f + n) are SLOT_T[t .. t + n)
+struct DevRun {
+  int32_t t;
+  int16_t f;
+  int16_t n;
 };
 
 // PLR storage on the device.  For each leaf the factors are stored as
@@ -103,9 +127,10 @@ struct DevSlot {     // one Vt row, for the t-phase
 };
 
 constexpr int PLR_TILE = 16;           // rows of a Y_PLR task
-constexpr int MAX_TILE_ENTRIES = 256;  // leaf entries of one Y_PLR task (all terms)
-constexpr int MAX_TCOLS = 1024;        // flat rank columns of one Y_PLR task
-constexpr int MAX_T_SLOTS = 512;       // Vt rows of one T_PLR task
+// per-task staging limits of the executor's task slots (defaults; the handle
+// sizes its slots from the operator, see pt_create)
+constexpr int MAX_T_SLOTS = 256;  // Vt rows (items) of one T_PLR task
+constexpr int MAX_TCOLS = 256;    // source columns a T_PLR task stages (or its widest Vt row)
 
 struct DevKernelPLR {
   int32_t leaf0, nleaf;      // into the leaf table

@@ -61,9 +61,12 @@ class DeviceOperator:
                  factors=None, device=None):
         torch = _torch()
         lib = nat.lib()
-        if not torch.cuda.is_available():
-            raise RuntimeError("DeviceOperator needs a CUDA device (no CPU fallback)")
-        self.device = torch.cuda.current_device() if device is None else int(device)
+        if device == "host":  # plan-only handle: host tables, pt_plan_stats (no GPU)
+            self.device = nat.PT_DEVICE_HOST
+        else:
+            if not torch.cuda.is_available():
+                raise RuntimeError("DeviceOperator needs a CUDA device (no CPU fallback)")
+            self.device = torch.cuda.current_device() if device is None else int(device)
         self.m = int(m)
         self.n_block_rows = int(n_block_rows)
         self.N = self.m * self.n_block_rows
@@ -131,6 +134,16 @@ class DeviceOperator:
         from .capture import capture_operator
         meta, arr = capture_operator(pol, perm)
         return cls.from_arrays(meta, arr, device=device)
+
+    PLAN_STATS = ("tasks", "t_plr", "y_plr", "y_dense", "pieces", "items", "counters",
+                  "algo_bytes", "staged_bytes", "max_terms", "max_pieces", "max_items")
+
+    def plan_stats(self, kind="AM", n_it=2):
+        """Host-side plan of one program (no launch): task / piece / byte counts."""
+        kinds = {"A": 0, "M": 1, "AM": 2, "S": 3}
+        st = (C.c_int64 * len(self.PLAN_STATS))()
+        nat.check(nat.lib().pt_plan_stats(self._h, kinds[kind], int(n_it), st), "pt_plan_stats")
+        return dict(zip(self.PLAN_STATS, (int(v) for v in st)))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -1,0 +1,83 @@
+"""Host-side program plans, no GPU (pt_create with PT_DEVICE_HOST + pt_plan_stats).
+
+The plan builder is the executor's compiler: it splits every operator apply
+into dataflow tasks, stages the operator in ring pieces and sizes the task
+slots.  These checks hold for any operator:
+- every program kind plans, and its task types add up;
+- the operator pieces stream exactly the algorithmic bytes once (each
+  kernel of an A-apply once; each D/R kernel of a sweep once per sweep);
+- per-task metadata stays within the executor's slot limits;
+- a plan-only handle refuses device work with PT_EINVAL.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import FIXTURES, case_path, golden_path
+from paper_1410_5910_b200 import _native as nat
+from paper_1410_5910_b200.operator import DeviceOperator, load_case_arrays
+
+
+def host_op(name):
+    path = golden_path(name) if name.startswith("fx_") else case_path(name)
+    if not path.exists():
+        pytest.skip(f"{path.name} not built")
+    meta, arr = load_case_arrays(path)
+    return DeviceOperator.from_arrays(meta, arr, device="host")
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_every_program_plans(name):
+    op = host_op(name)
+    for kind, n_it in (("A", 0), ("M", 1), ("M", 2), ("AM", 2), ("S", 0)):
+        st = op.plan_stats(kind, n_it)
+        assert st["tasks"] > 0
+        assert st["t_plr"] + st["y_plr"] + st["y_dense"] == st["tasks"]
+        assert st["counters"] >= 1
+        if op.kernel_format == "dense":
+            assert st["t_plr"] == st["y_plr"] == st["items"] == 0
+        else:
+            assert st["t_plr"] > 0 and st["y_plr"] > 0
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_pieces_stream_the_algorithmic_bytes(name):
+    op = host_op(name)
+    a = op.plan_stats("A")
+    assert a["staged_bytes"] == a["algo_bytes"] > 0
+    m1 = op.plan_stats("M", 1)
+    m2 = op.plan_stats("M", 2)
+    # the second sweep re-reads every D/R kernel once more
+    assert m2["staged_bytes"] > m1["staged_bytes"]
+    am = op.plan_stats("AM", 2)
+    assert am["staged_bytes"] == a["staged_bytes"] + m2["staged_bytes"]
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_task_metadata_within_slot_limits(name):
+    op = host_op(name)
+    for kind in ("A", "AM"):
+        st = op.plan_stats(kind, 2)
+        assert st["max_terms"] <= 16
+        assert st["max_pieces"] <= 48
+
+
+def test_plan_only_handle_refuses_device_work():
+    op = host_op(FIXTURES[0])
+    x = np.zeros(op.N * 2)
+    rc = nat.lib().pt_apply_A(op._h, x.ctypes.data, x.ctypes.data, None)
+    assert rc == nat.PT_EINVAL
+    assert b"plan-only" in nat.lib().pt_last_error()
+    g, sm, he = C.c_int32(), C.c_int64(), C.c_int64()
+    assert nat.lib().pt_exec_info(op._h, C.byref(g), C.byref(sm), C.byref(he)) == 0
+    assert g.value % 148 == 0 and 0 < sm.value <= 232448 and he.value > 0
+
+
+@pytest.mark.parametrize("name", ["c1", "c3r", "c2", "c3"])
+def test_large_case_plans(name):
+    """Reference-scale operators (when cases/ holds them) plan within limits."""
+    op = host_op(name)
+    st = op.plan_stats("AM", 2)
+    assert st["staged_bytes"] == op.plan_stats("A")["algo_bytes"] + op.plan_stats("M", 2)["algo_bytes"]

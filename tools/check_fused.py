@@ -19,7 +19,7 @@ for name in sys.argv[1:]:
     x = torch.from_numpy(np.array(arr["probe_x"])).cuda()
     ref = op.apply_M(op.apply_A(x))
     cap = 1 << 20
-    rec = np.zeros(cap * 12, dtype=np.int64)
+    rec = np.zeros(cap * 32, dtype=np.int64)
     n = C.c_int64()
     errs = []
     for rep in range(6):

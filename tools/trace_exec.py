@@ -24,17 +24,18 @@ from paper_1410_5910_b200.operator import DeviceOperator, load_case_arrays  # no
 
 KIND = {"A": 0, "M": 1, "AM": 2, "S": 3}
 TYPES = {0: "Ydense", 1: "Yplr", 2: "Tplr"}
+W = 32  # PT_TRACE_WORDS
 
 
 def trace(op, kind, x, n_it=2):
     y = torch.empty_like(x)
     cap = 1 << 20
-    rec = np.zeros(cap * 12, dtype=np.int64)
+    rec = np.zeros(cap * W, dtype=np.int64)
     n = C.c_int64()
     rc = nat.lib().pt_trace_program(op.handle, KIND[kind], n_it, x.data_ptr(), y.data_ptr(),
                                     rec.ctypes.data_as(C.POINTER(C.c_int64)), cap, C.byref(n))
     nat.check(rc, "trace")
-    return rec[: n.value * 12].reshape(n.value, 12)
+    return rec[: n.value * W].reshape(n.value, W)
 
 
 def summarize(r, label):
@@ -42,13 +43,19 @@ def summarize(r, label):
     grab, ready, done = (r[:, 6] - t0) / 1e3, (r[:, 7] - t0) / 1e3, (r[:, 8] - t0) / 1e3
     span = done.max()
     print(f"== {label}: {len(r)} tasks, launch span {span:.1f} us")
+    p0 = np.where(r[:, 10] > 0, (r[:, 10] - t0) / 1e3, np.nan)
     for ty in sorted(set(r[:, 0])):
         sel = r[:, 0] == ty
         busy = (done - ready)[sel]
         wait = (ready - grab)[sel]
+        # time after the dependency wait until the first operator piece was in smem
+        pw = np.nanmean(np.maximum(p0[sel] - ready[sel], 0)) if np.isfinite(p0[sel]).any() else 0
+        # piece-0 latency from issue (grab) to arrival
+        pl = np.nanmean(p0[sel] - grab[sel]) if np.isfinite(p0[sel]).any() else 0
         print(f"  {TYPES.get(int(ty), ty):7s} n={sel.sum():5d} busy mean {busy.mean():6.2f} us "
               f"max {busy.max():6.2f}  sum {busy.sum():9.1f} | wait mean {wait.mean():6.2f} "
-              f"max {wait.max():6.2f}")
+              f"max {wait.max():6.2f} | piece0 arrives {pl:5.2f} after grab, "
+              f"{pw:5.2f} after ready")
     nbins = 40
     edges = np.linspace(0, span, nbins + 1)
     act = []
@@ -82,9 +89,32 @@ def main():
         trace(op, k, x)  # warm
         r = trace(op, k, x)
         summarize(r, f"{args.case} {k}")
+        phases(r, f"{args.case} {k}")
         res[k] = r
     if args.out:
         np.savez(args.out, **res)
+
+
+
+
+def phases(r, label):
+    """Mean in-task phase durations (us) per task type from the marks."""
+    print(f"-- {label} in-task phases (mean us)")
+    us = lambda a, b: np.where((a > 0) & (b > 0), (a - b) / 1e3, np.nan)  # noqa: E731
+    for ty in sorted(set(r[:, 0])):
+        rr = r[r[:, 0] == ty]
+        ready, staged, cstart, done = rr[:, 7], rr[:, 12], rr[:, 10], rr[:, 8]
+        issue, landed = rr[:, 14:22], rr[:, 22:30]
+        lat = np.nanmean(us(landed, issue))
+        gaps = np.nanmean(us(landed[:, 1:], landed[:, :-1]))
+        pre = np.nanmean(np.where(issue[:, 0] > 0, (issue[:, 0] < ready), np.nan))
+        print(f"   {TYPES.get(int(ty), ty):7s} pieces {rr[:, 13].mean():5.1f} | ready->staged "
+              f"{np.nanmean(us(staged, ready)):5.2f} | staged->consumers "
+              f"{np.nanmean(us(cstart, staged)):5.2f} | consumers busy {np.nanmean(us(done, cstart)):5.2f} "
+              f"| piece issue->seen {lat:5.2f} | gap between pieces seen {gaps:5.2f} | "
+              f"piece0 issued before ready {pre:4.2f} | consumer cycles: wait pieces "
+              f"{rr[:, 30].mean():7.0f} barrier {rr[:, 31].mean():7.0f} "
+              f"(of {np.nanmean(us(done, cstart)) * 1.9e3:7.0f})")
 
 
 if __name__ == "__main__":
