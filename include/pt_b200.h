@@ -210,7 +210,8 @@ int pt_plan_stats(pt_handle *h, int32_t kind, int32_t n_it, int64_t *stats);
 /* ---- misc ----------------------------------------------------------------*/
 const char *pt_last_error(void);
 int32_t pt_abi_version(void);
-/* number of kernel launches issued by this library since load */
+/* number of kernels this library has launched since load (the nodes of
+ * graph-resident solves are counted per execution) */
 int64_t pt_launch_count(void);
 /* algorithmic bytes of one A-apply / one n_it-sweep preconditioner apply
  * (distinct kernels read once) */

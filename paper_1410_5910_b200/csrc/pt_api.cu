@@ -145,6 +145,7 @@ struct pt_handle {
   struct SolveGraph {
     int n_it = 0, max_iter = 0;
     double tol = 0.0;
+    int64_t k_pro = 0, k_body = 0, k_epi = 0;  // kernel nodes per part
     cudaGraphExec_t exec = nullptr;
   };
   std::vector<SolveGraph> graphs;
@@ -525,7 +526,7 @@ int ws_alloc(pt_gmres_ws* w, int64_t n, int max_iter) {
   d.ldp = max_iter + 2;
   const size_t ldr = (size_t)max_iter + 1;
   CK(cudaMalloc(&d.V, (size_t)n * ldr * sizeof(double2)));
-  CK(cudaMalloc(&d.P, (size_t)RED_BLOCKS * d.ldp * sizeof(double2)));
+  CK(cudaMalloc(&d.P, 2 * (size_t)RED_BLOCKS * d.ldp * sizeof(double2)));
   CK(cudaMalloc(&d.h1, (max_iter + 2) * sizeof(double2)));
   CK(cudaMalloc(&d.h2, (max_iter + 2) * sizeof(double2)));
   CK(cudaMalloc(&d.hn2, 2 * sizeof(double2)));
@@ -544,6 +545,7 @@ int ws_alloc(pt_gmres_ws* w, int64_t n, int max_iter) {
   CK(cudaMemset(d.nonfinite, 0, sizeof(int)));
   CK(cudaMemset(d.ticket, 0, 4 * sizeof(int)));
   for (auto& e : w->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(gm_arnoldi_setup(d, w->device));
   return 0;
 }
 
@@ -580,7 +582,7 @@ int ws_step_impl(pt_gmres_ws* w, int j, double rel_tol, int max_iter, pt_report*
   GmresDev& d = w->d;
   if (j < 0 || j >= d.max_iter || max_iter > d.max_iter)
     return fail(PT_EINVAL, "GMRES step index outside the workspace");
-  gm_arnoldi_step(d, rel_tol, max_iter, 0, s);
+  CK(gm_arnoldi_step(d, rel_tol, max_iter, 0, s));
   CK(cudaGetLastError());
   int rc = fetch_status(w, s);
   if (rc) return rc;
@@ -886,6 +888,9 @@ int build_solve_graph(pt_handle* h, int n_it, int max_iter, double tol,
   CK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle cond;
   CK(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+  // kernel launches counted per part; a capture launches nothing, the
+  // graph's executions are counted when it runs (gmres_graph)
+  const int64_t c0 = g_launches.load();
   // prologue
   CK(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   rc = run_program(h, pM, h->gb, d.V, nullptr, cs);
@@ -906,6 +911,7 @@ int build_solve_graph(pt_handle* h, int n_it, int max_iter, double tol,
   cp.conditional.size = 1;
   cudaGraphNode_t loop;
   CK(cudaGraphAddNode(&loop, g, tail.data(), tail.size(), &cp));
+  const int64_t c1n = g_launches.load();
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal));
@@ -914,9 +920,11 @@ int build_solve_graph(pt_handle* h, int n_it, int max_iter, double tol,
   im.vbase = d.V;
   im.vstride = d.n;
   rc = run_program(h, pAM, nullptr, nullptr, nullptr, cs, &d.st->stop, im);
-  if (!rc) gm_arnoldi_step(d, tol, max_iter, cond, cs);
+  cudaError_t ae = rc ? cudaSuccess : gm_arnoldi_step(d, tol, max_iter, cond, cs);
   CK(cudaStreamEndCapture(cs, &tmp));
   if (rc) return rc;
+  CK(ae);
+  const int64_t c2n = g_launches.load();
   // epilogue
   CK(cudaStreamBeginCaptureToGraph(cs, g, &loop, nullptr, 1, cudaStreamCaptureModeThreadLocal));
   gm_finish(d, h->gx, cs);
@@ -931,6 +939,11 @@ int build_solve_graph(pt_handle* h, int n_it, int max_iter, double tol,
   CK(c2);
   CK(cudaGraphInstantiate(&out->exec, g, 0));
   CK(cudaGraphDestroy(g));
+  const int64_t c3n = g_launches.load();
+  out->k_pro = c1n - c0;
+  out->k_body = c2n - c1n;
+  out->k_epi = c3n - c2n;
+  g_launches.fetch_sub(c3n - c0);
   out->n_it = n_it;
   out->max_iter = max_iter;
   out->tol = tol;
@@ -984,13 +997,14 @@ int gmres_graph(pt_handle* h, const double2* b, double2* x, bool b_host, bool x_
   if (b != h->gb)
     CK(cudaMemcpyAsync(h->gb, b, bytes, b_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                        s));
-  count_launch();
   CK(cudaGraphLaunch(sg->exec, s));
   if (x != h->gx)
     CK(cudaMemcpyAsync(x, h->gx, bytes, x_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
                        s));
   CK(cudaStreamSynchronize(s));
   const DevStatus st = h->gws->st_host[0];
+  // kernels the graph ran: prologue, one body per iteration, epilogue
+  g_launches.fetch_add(sg->k_pro + (int64_t)st.iterations * sg->k_body + sg->k_epi);
   if (rep->residual_history && st.iterations > 0)
     std::memcpy(rep->residual_history, h->hist_host, (size_t)st.iterations * sizeof(double));
   return finish_report(h, st, cfg->max_iter, rep);
@@ -1023,7 +1037,7 @@ int gmres_stream(pt_handle* h, const double2* b, double2* x, const pt_gmres_conf
     for (int i = 0; i < B && enq < cfg->max_iter; ++i, ++enq) {
       int r = run_program(h, pAM, nullptr, nullptr, nullptr, s, &d.st->stop, im);
       if (r) return r;
-      gm_arnoldi_step(d, cfg->rel_tol, cfg->max_iter, 0, s);
+      CK(gm_arnoldi_step(d, cfg->rel_tol, cfg->max_iter, 0, s));
     }
     CK(cudaMemcpyAsync(w->st_host + (nb % 2), d.st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(w->ev[nb % 2], s));

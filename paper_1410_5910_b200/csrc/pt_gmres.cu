@@ -9,11 +9,16 @@
 // out of one rotation instead of a least-squares solve.  The flag logic
 // (breakdown, tolerance, stagnation window, maxiter) follows :265-289.
 //
-// Each Arnoldi step is four kernels.  Block partial sums are reduced by the
-// last block to finish (ticket counter), always over all blocks in index
-// order, so results are bitwise repeatable.  Every step kernel returns at
+// Each Arnoldi step is one cooperative kernel, one block per SM, with three
+// grid-wide barriers (after h1, h2 and ||w|| partials).  Every block reduces
+// the block partials itself in the same fixed order, so all blocks hold the
+// same coefficients and results are bitwise repeatable.  The begin / finish
+// kernels reduce partials in the last block to finish (ticket counter).  Every step kernel returns at
 // once when the status says the solve has stopped: the host enqueues steps
 // ahead of its convergence check without changing the result.
+#include <cooperative_groups.h>
+
+#include <atomic>
 #include <cmath>
 
 #include "pt_device.cuh"
@@ -197,6 +202,140 @@ __device__ void givens_update(const GmresDev& g, int j, double rel_tol, int max_
     st->stop = 1;
   }
   __threadfence();
+}
+
+// ---- fused Arnoldi step ---------------------------------------------------------
+
+namespace cg = cooperative_groups;
+
+// out[c] = sum over blocks b (index order) of P[b * ldp + c], c < nc, by
+// groups of 8 threads per column (partials b = sub mod 8 in order, then a
+// fixed xor tree): the same result in every block
+__device__ void arn_reduce(const double2* P, int ldp, int nblk, int nc, double2* out) {
+  const int sub = threadIdx.x & 7;
+  for (int c0 = 0; c0 < nc; c0 += ARN_THREADS / 8) {
+    const int c = c0 + (int)threadIdx.x / 8;
+    double2 s = make_double2(0.0, 0.0);
+    if (c < nc)
+      for (int b = sub; b < nblk; b += 8) s = cadd(s, ld_cg(P + (int64_t)b * ldp + c));
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    }
+    if (c < nc && sub == 0) out[c] = s;
+  }
+}
+
+// P[blockIdx.x, c] = sum_{e in slice} conj(V_c[e]) w[e]; warp per column,
+// the block's slice of w in shared memory
+__device__ void arn_dots(const double2* V, int64_t ldv, int nc, const double2* ws, int64_t lo,
+                         int len, double2* Prow) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < nc; c += ARN_THREADS / 32) {
+    const double2* v = V + (int64_t)c * ldv + lo;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int e = lane; e < len; e += 32) acc = cfma_conj(ld_cg(v + e), ws[e], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) st_cg(Prow + c, acc);
+  }
+}
+
+// ws[e] -= sum_c V_c[e] h[c] over the block's slice (thread per element)
+__device__ void arn_update(const double2* V, int64_t ldv, int nc, const double2* h, double2* ws,
+                           int64_t lo, int len) {
+  for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int c = 0; c < nc; ++c) acc = cfma(ld_cg(V + (int64_t)c * ldv + lo + e), h[c], acc);
+    ws[e] = csub(ws[e], acc);
+  }
+}
+
+// w = basis column j+1 (written by the preconditioned matvec): CGS2 against
+// columns 0..j, ||w||, Givens + flags (block 0), w /= ||w|| (every block).
+__global__ void __launch_bounds__(ARN_THREADS, 1)
+k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle cond) {
+  extern __shared__ double2 sm[];
+  if (stopped(g.st)) return;  // uniform: no block reaches a grid barrier
+  cg::grid_group grid = cg::this_grid();
+  const int j = g.st->iterations;
+  const int nc = j + 1;
+  const int nblk = gridDim.x;
+  const int64_t chunk = (g.n + nblk - 1) / nblk;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int len = (int)(lo + chunk < g.n ? chunk : (lo < g.n ? g.n - lo : 0));
+  double2* hsm = sm;                  // coefficients (ldp)
+  double2* ws = sm + g.ldp;           // the block's slice of w
+  double2* w = g.V + (int64_t)(j + 1) * g.n;
+  double2* P1 = g.P;
+  double2* P2 = g.P + (int64_t)RED_BLOCKS * g.ldp;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  int bad = 0;
+  for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
+    const double2 v = ld_cg(w + lo + e);
+    bad |= !(isfinite(v.x) && isfinite(v.y));
+    ws[e] = v;
+  }
+  if (bad) atomicOr(&s_bad, 1);
+  __syncthreads();
+  if (s_bad && threadIdx.x == 0) atomicOr(g.nonfinite, 1);
+  // pass 1: h1 = V^H w
+  arn_dots(g.V, g.n, nc, ws, lo, len, P1 + (int64_t)blockIdx.x * g.ldp);
+  grid.sync();
+  arn_reduce(P1, g.ldp, nblk, nc, hsm);
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < nc; c += ARN_THREADS) st_cg(g.h1 + c, hsm[c]);
+  __syncthreads();
+  // pass 2: w -= V h1, h2 = V^H w
+  arn_update(g.V, g.n, nc, hsm, ws, lo, len);
+  __syncthreads();
+  arn_dots(g.V, g.n, nc, ws, lo, len, P2 + (int64_t)blockIdx.x * g.ldp);
+  grid.sync();
+  arn_reduce(P2, g.ldp, nblk, nc, hsm);
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < nc; c += ARN_THREADS) st_cg(g.h2 + c, hsm[c]);
+  __syncthreads();
+  // w -= V h2, ||w||^2
+  arn_update(g.V, g.n, nc, hsm, ws, lo, len);
+  {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
+      const double2 v = ws[e];
+      acc.x = fma(v.x, v.x, acc.x);
+      acc.x = fma(v.y, v.y, acc.x);
+    }
+    __shared__ double2 red[ARN_THREADS / 32];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int i = 0; i < ARN_THREADS / 32; ++i) s = cadd(s, red[i]);
+      st_cg(P1 + (int64_t)blockIdx.x * g.ldp, s);  // P1 is free: pass-1 partials consumed
+    }
+  }
+  grid.sync();
+  arn_reduce(P1, g.ldp, nblk, 1, hsm);
+  __syncthreads();
+  const double hn = sqrt(hsm[0].x);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st_cg(g.hn2, hsm[0]);
+    __threadfence();
+    givens_update(g, j, rel_tol, max_iter);
+    if (cond) cudaGraphSetConditional(cond, g.st->stop ? 0u : 1u);
+  }
+  // v_{j+1} = w / ||w|| (unused when the solve stops here; breakdown => 0)
+  const double inv = hn <= BREAKDOWN_REL * g.st->beta ? 0.0 : 1.0 / hn;
+  for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
+    double2 v = ws[e];
+    v.x *= inv;
+    v.y *= inv;
+    st_cg(w + lo + e, v);
+  }
 }
 
 // ---- kernels -----------------------------------------------------------------
@@ -399,17 +538,43 @@ int grid_for(int64_t n) {
 
 }  // namespace
 
-void gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
-                     cudaGraphConditionalHandle cond, cudaStream_t s) {
-  const size_t hs = (size_t)(g.max_iter + 1) * sizeof(double2);
+cudaError_t gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
+                            cudaGraphConditionalHandle cond, cudaStream_t s) {
+  const int64_t chunk = (g.n + g.arn_blocks - 1) / g.arn_blocks;
+  const size_t smem = (size_t)(g.ldp + chunk) * sizeof(double2);
   count_launch();
-  k_h1<<<RED_BLOCKS, RED_THREADS, 0, s>>>(g);
-  count_launch();
-  k_h2<<<RED_BLOCKS, RED_THREADS, hs, s>>>(g);
-  count_launch();
-  k_norm_givens<<<RED_BLOCKS, RED_THREADS, hs, s>>>(g, rel_tol, max_iter, cond);
-  count_launch();
-  k_normalize<<<grid_for(g.n), 256, 0, s>>>(g);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.arn_blocks);
+  cfg.blockDim = dim3(ARN_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_arnoldi, g, rel_tol, max_iter, cond);
+}
+
+cudaError_t gm_arnoldi_setup(GmresDev& g, int device) {
+  int nsm = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return e;
+  g.arn_blocks = nsm < ARN_MAX_BLOCKS ? nsm : ARN_MAX_BLOCKS;
+  const int64_t chunk = (g.n + g.arn_blocks - 1) / g.arn_blocks;
+  const size_t smem = (size_t)(g.ldp + chunk) * sizeof(double2);
+  // per-function attribute shared by every workspace: it only grows
+  static std::atomic<int> attr_max{0};
+  int cur = attr_max.load();
+  while ((int)smem > cur && !attr_max.compare_exchange_weak(cur, (int)smem)) {
+  }
+  e = cudaFuncSetAttribute(k_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           cur > (int)smem ? cur : (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi, ARN_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  return occ >= 1 ? cudaSuccess : cudaErrorInvalidConfiguration;
 }
 
 void gm_begin(const GmresDev& g, cudaGraphConditionalHandle cond, cudaStream_t s) {

@@ -8,6 +8,8 @@ namespace pt {
 constexpr int RED_THREADS = 256;
 constexpr int RED_BLOCKS = 296;  // fixed partial count => deterministic sums
 constexpr int RED_CHUNK = 8;     // basis columns per pass of the dot kernel
+constexpr int ARN_THREADS = 512; // fused Arnoldi step: threads per block
+constexpr int ARN_MAX_BLOCKS = RED_BLOCKS;
 
 // STAGNATION_WINDOW / STAGNATION_IMPROVEMENT of solver.py:55-56
 constexpr int STAG_WINDOW = 10;
@@ -33,8 +35,9 @@ struct GmresDev {
   int64_t n;
   int max_iter;
   int ldp;            // partial row stride (>= max_iter + 2)
+  int arn_blocks;     // blocks of the fused Arnoldi step (one per SM, co-resident)
   double2* V;         // n x (max_iter + 1), column j at V + j*n
-  double2* P;         // RED_BLOCKS x ldp partials
+  double2* P;         // 2 x RED_BLOCKS x ldp partials
   double2* h1;        // CGS pass 1 coefficients
   double2* h2;        // CGS pass 2 coefficients
   double2* hn2;       // [0].x = ||w||^2
@@ -59,8 +62,11 @@ struct GmresDev {
 // One Arnoldi step (w = basis column j+1):
 //   h1 = V^H w (+ non-finite check) | w -= V h1, h2 = V^H w |
 //   w -= V h2, ||w||, Givens + flags | w /= ||w||
-void gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
-                     cudaGraphConditionalHandle cond, cudaStream_t s);
+// One cooperative kernel (grid-wide barriers between the reductions).
+cudaError_t gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
+                            cudaGraphConditionalHandle cond, cudaStream_t s);
+// blocks / shared memory of the fused step for this workspace (once)
+cudaError_t gm_arnoldi_setup(GmresDev& g, int device);
 // ||V0||, beta, g = beta e1, V0 /= beta; stop if beta == 0
 void gm_begin(const GmresDev& g, cudaGraphConditionalHandle cond, cudaStream_t s);
 // y = R^-1 g, x = V[:, :k] y (k = st->iterations)

@@ -25,6 +25,7 @@ for _ in range(reps):
     elif kind == "M":
         op.apply_M(x, out=y)
     else:
-        op.gmres(torch.from_numpy(np.array(arr["rhs"][0])).cuda(), rel_tol=1e-9, max_iter=2)
+        op.gmres(torch.from_numpy(np.array(arr["rhs"][0])).cuda(), rel_tol=1e-9,
+                 max_iter=int(sys.argv[4]) if len(sys.argv) > 4 else 2)
 torch.cuda.synchronize()
 print("ok", kind, float(y.abs().sum()))
