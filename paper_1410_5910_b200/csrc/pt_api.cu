@@ -767,6 +767,8 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     int cur = attr_max.load();
     while ((int)h->smem > cur && !attr_max.compare_exchange_weak(cur, (int)h->smem)) {
     }
+    CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            (int)cudaSharedmemCarveoutMaxShared));
     CK(cudaFuncSetAttribute(pt_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             std::max(cur, (int)h->smem)));
     int occ = 0;

@@ -252,9 +252,9 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
   bytes = (bytes + (uint32_t)(nk * nrows)) * (uint32_t)sizeof(double2);
   if (bytes == 0) return;
   const uint32_t phase = (uint32_t)(n_staged++ & 1);
+  // sources written by other CTAs (generic proxy) are read by the TMA
+  asm volatile("fence.proxy.async.global;" ::: "memory");
   if (lane == 0) {
-    // sources written by other CTAs (generic proxy) are read by the TMA
-    asm volatile("fence.proxy.async.global;" ::: "memory");
     asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_stg[k])),
                  "r"(bytes)
                  : "memory");
@@ -345,11 +345,19 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
         while (issued < t.npiece && stage_free(L, seq)) issue_piece(a, L, sl, q, issued++, seq++);
         s_seq = seq;
       }
-      const DevWait* w = sl.waits();
-      for (int i = 0; i < t.nwait; ++i)  // dependencies
-        while (ld_acquire(a.ctr + w[i].ctr) < w[i].val) __nanosleep(20);
-      trace_mark(a, q, 1);
     }
+    {  // dependencies: the lanes poll the task's counters in parallel
+      const DevWait* w = sl.waits();
+      bool ok = true;
+      do {
+        ok = true;
+        for (int i = lane; i < t.nwait; i += 32)
+          if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
+        ok = __all_sync(0xffffffffu, ok);
+        if (!ok) __nanosleep(20);
+      } while (!ok);
+    }
+    if (lane == 0) trace_mark(a, q, 1);
     __syncwarp();
     stage_vectors(a, t, sl, k, n_staged, lane);
     __syncwarp();

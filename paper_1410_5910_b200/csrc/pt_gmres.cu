@@ -571,6 +571,15 @@ cudaError_t gm_arnoldi_setup(GmresDev& g, int device) {
   e = cudaFuncSetAttribute(k_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            cur > (int)smem ? cur : (int)smem);
   if (e != cudaSuccess) return e;
+  // every kernel of the solve prefers the executor's shared-memory carveout:
+  // no SM reconfiguration between the graph's kernels
+  for (const void* f : {(const void*)k_arnoldi, (const void*)k_begin_norm, (const void*)k_begin_scale,
+                        (const void*)k_backsolve, (const void*)k_combine, (const void*)k_resid,
+                        (const void*)k_zero}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+  }
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi, ARN_THREADS, smem);
   if (e != cudaSuccess) return e;

@@ -63,10 +63,9 @@ class Builder {
   int emit_block(VecRef out, const std::vector<TermSpec>& terms,
                  const std::vector<EyeSpec>& eyes, bool has_init, VecRef init,
                  bool has_rhs, VecRef rhs, double rhs_coef) {
+    // waits every output task of the block has (t-vectors, dense sources);
+    // the row-local inputs (eyes, init, rhs) are added per task
     std::vector<int> waits;
-    for (const EyeSpec& e : eyes) add_wait(waits, e.src);
-    if (has_init) add_wait(waits, init);
-    if (has_rhs) add_wait(waits, rhs);
     const int32_t term0 = (int32_t)prog_.terms.size();
     const bool plr = op_.fmt == 1 && !terms.empty();
     double ybytes = 0.0;
@@ -83,9 +82,8 @@ class Builder {
       if (plr) {
         const int32_t ns = op_.nslot[t.kernel];
         dt.t_base = alloc_t(ns);
-        // T tasks: t = Vt (sum of sources), warp per slot
-        std::vector<int> twaits;
-        for (const VecRef& s : t.src) add_wait(twaits, s);
+        // T tasks: t = Vt (sum of sources); each waits only for the source
+        // rows its slice [c0, c1) reads
         const int g = new_group();
         const int32_t term_idx = (int32_t)prog_.terms.size();
         const DevKernelPLR& kp = op_.kplr[t.kernel];
@@ -165,6 +163,8 @@ class Builder {
           tk.nitem = (int32_t)prog_.items.size() - tk.item0;
           if (tk.nitem > pp_.item_cap) flag("a T task has more slots than a task slot holds");
           if (tk.c1 - tk.c0 > pp_.tcols_cap) flag("a Vt row is wider than a task slot stages");
+          std::vector<int> twaits;
+          for (const VecRef& sv : t.src) add_wait_rows(twaits, sv, tk.c0, tk.c1);
           push_task(tk, twaits, g, 16.0 * (double)total);
           s0 = s1;
         }
@@ -185,10 +185,17 @@ class Builder {
       de.src = e.src;
       prog_.eyes.push_back(de);
     }
-    const int g = new_group();
+    // output rows are published in chunks of ROW_CHUNK rows (one producer
+    // group each), so consumers of a row range start before the block ends
     const int64_t m = op_.m;
     const int rpt = plr ? pp_.plr_rows_per_task : pp_.dense_rows_per_task;
+    const int64_t chunk_rows = std::max<int64_t>(ROW_CHUNK / rpt, 1) * rpt;
+    int g = -1;
     for (int64_t r0 = 0; r0 < m; r0 += rpt) {
+      if (r0 % chunk_rows == 0) {
+        g = new_group();
+        register_producer_rows(out, r0, std::min<int64_t>(m, r0 + chunk_rows), g);
+      }
       DevTask tk{};
       tk.piece0 = (int32_t)prog_.pieces.size();
       if (plr) {  // one item per flat (leaf, rank column) of all terms, pieces of whole columns
@@ -264,9 +271,12 @@ class Builder {
       tk.has_rhs = has_rhs ? 1 : 0;
       tk.rhs = rhs;
       tk.rhs_coef = rhs_coef;
-      push_task(tk, waits, g, ybytes * double(tk.r1 - tk.r0) / double(m));
+      std::vector<int> tw = waits;
+      for (const EyeSpec& e : eyes) add_wait_rows(tw, e.src, tk.r0, tk.r1);
+      if (has_init) add_wait_rows(tw, init, tk.r0, tk.r1);
+      if (has_rhs) add_wait_rows(tw, rhs, tk.r0, tk.r1);
+      push_task(tk, tw, g, ybytes * double(tk.r1 - tk.r0) / double(m));
     }
-    register_producer(out, g);
     return g;
   }
 
@@ -385,15 +395,29 @@ class Builder {
     return g.ctr;
   }
 
+  // producer groups of a vector block, by row range (a later producer of the
+  // same block replaces the earlier ones)
+  struct RowGroup {
+    int64_t lo, hi;
+    int g;
+  };
   void register_producer(VecRef block, int g) {
-    producer_[std::make_pair(block.slot, block.off)] = g;
+    producer_[std::make_pair(block.slot, block.off)] = {RowGroup{0, INT64_MAX, g}};
+  }
+  void register_producer_rows(VecRef block, int64_t lo, int64_t hi, int g) {
+    auto& v = producer_[std::make_pair(block.slot, block.off)];
+    if (lo == 0) v.clear();
+    v.push_back(RowGroup{lo, hi, g});
   }
 
-  void add_wait(std::vector<int>& waits, VecRef r) {
+  void add_wait(std::vector<int>& waits, VecRef r) { add_wait_rows(waits, r, 0, INT64_MAX); }
+  // wait for the producers of rows [lo, hi) of block r
+  void add_wait_rows(std::vector<int>& waits, VecRef r, int64_t lo, int64_t hi) {
     auto it = producer_.find(std::make_pair(r.slot, r.off));
     if (it == producer_.end()) return;
-    if (std::find(waits.begin(), waits.end(), it->second) == waits.end())
-      waits.push_back(it->second);
+    for (const RowGroup& rg : it->second)
+      if (rg.lo < hi && lo < rg.hi && std::find(waits.begin(), waits.end(), rg.g) == waits.end())
+        waits.push_back(rg.g);
   }
 
   int64_t alloc_t(int64_t n) {
@@ -414,7 +438,7 @@ class Builder {
   const Operator& op_;
   PlanParams pp_;
   Program prog_;
-  std::map<std::pair<int32_t, int64_t>, int> producer_;
+  std::map<std::pair<int32_t, int64_t>, std::vector<RowGroup>> producer_;
   std::vector<Group> groups_;
   std::vector<std::vector<int>> task_waits_;
   std::vector<int> task_group_;
@@ -468,6 +492,9 @@ void emit_sweep(Builder& b, const Operator& op, VecRef rhs, bool has_uold, VecRe
                 VecRef unew, VecRef pre) {
   const int64_t m = op.m, nt = op.nt;
   b.begin_stage();
+  // small T tasks for the whole sweep: its pre-phase tasks share CTAs with
+  // the chain and must not hold a CTA's consumers long
+  b.t_pieces_now = b.params().t_pieces_chain;
   b.need_slot(unew.slot, unew.off + op.nb * m);
   b.need_slot(pre.slot, pre.off + op.nb * m);
   // rows[h][p]: entries of half-row p
@@ -559,9 +586,8 @@ void emit_sweep(Builder& b, const Operator& op, VecRef rhs, bool has_uold, VecRe
       }
     }
   }
-  // chain, level by level, both halves interleaved; small T tasks: a level's
-  // t-phase spreads over all CTAs (its latency is on the critical path)
-  b.t_pieces_now = b.params().t_pieces_chain;
+  // chain, level by level, both halves interleaved (small T tasks: a level's
+  // t-phase spreads over all CTAs; its latency is on the critical path)
   for (int lv = 0; lv <= max_level; ++lv) {
     for (int h = 0; h < 2; ++h) {
       for (int64_t q = 0; q < nt; ++q) {

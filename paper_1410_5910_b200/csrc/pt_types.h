@@ -127,6 +127,7 @@ struct DevSlot {     // one Vt row, for the t-phase
 };
 
 constexpr int PLR_TILE = 16;           // rows of a Y_PLR task
+constexpr int ROW_CHUNK = 64;          // output rows published per producer group
 // per-task staging limits of the executor's task slots (defaults; the handle
 // sizes its slots from the operator, see pt_create)
 constexpr int MAX_T_SLOTS = 256;  // Vt rows (items) of one T_PLR task
