@@ -790,6 +790,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     h->pp.dense_rows_per_task = std::max(1, std::min(DENSE_RT_MAX, std::atoi(e)));
   if (const char* e = std::getenv("PT_T_SLOTS")) h->pp.plr_slots_per_task = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_T_PIECES")) h->pp.t_pieces = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PT_ROW_CHUNK")) h->pp.row_chunk = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
     h->pp.t_pieces_chain = std::max(1, std::atoi(e));
   if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));

@@ -305,9 +305,9 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     const int use = 2 * j + k;
     if (j > 0) {  // consumers done with use - 2: publish its outputs
       bar_wait(&s_tempty[k], (j - 1) & 1);
-      if (lane == 0) {
-        __threadfence();
-        atomicAdd(a.ctr + sl.desc().signal, 1);
+      if (lane == 0) {  // release: the consumers' outputs before the count
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.ctr + sl.desc().signal)
+                     : "memory");
       }
     }
     // one task per use, grabbed in use order (the CTA's uses run in

@@ -189,7 +189,7 @@ class Builder {
     // group each), so consumers of a row range start before the block ends
     const int64_t m = op_.m;
     const int rpt = plr ? pp_.plr_rows_per_task : pp_.dense_rows_per_task;
-    const int64_t chunk_rows = std::max<int64_t>(ROW_CHUNK / rpt, 1) * rpt;
+    const int64_t chunk_rows = std::max<int64_t>(pp_.row_chunk / rpt, 1) * rpt;
     int g = -1;
     for (int64_t r0 = 0; r0 < m; r0 += rpt) {
       if (r0 % chunk_rows == 0) {
