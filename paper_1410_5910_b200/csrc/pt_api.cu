@@ -791,6 +791,10 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_T_SLOTS")) h->pp.plr_slots_per_task = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_T_PIECES")) h->pp.t_pieces = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_ROW_CHUNK")) h->pp.row_chunk = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PT_CHAIN_BOOST")) h->pp.chain_boost_us = std::atof(e);
+  if (const char* e = std::getenv("PT_SIM_SLOTS")) h->pp.ctas = h->grid * std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PT_TASK_US")) h->pp.task_us = std::atof(e);
+  if (const char* e = std::getenv("PT_CTA_GBS")) h->pp.cta_gbs = std::atof(e);
   if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
     h->pp.t_pieces_chain = std::max(1, std::atoi(e));
   if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
@@ -1307,6 +1311,39 @@ int pt_plan_stats(pt_handle* h, int32_t kind, int32_t n_it, int64_t* stats) {
   stats[7] = (int64_t)pg.algo_bytes;
   for (const DevPiece& pc : pg.pieces) stats[8] += 16 * (int64_t)pc.elems;
   if (!pg.overflow.empty()) return fail(PT_EINVAL, pg.overflow);
+  return 0;
+}
+
+int pt_plan_tasks(pt_handle* h, int32_t kind, int32_t n_it, int32_t* rec, int64_t cap,
+                  int64_t* n_out) {
+  if (!h || !rec || !n_out) return fail(PT_EINVAL, "null argument");
+  if (kind < 0 || kind > 3) return fail(PT_EINVAL, "unknown program kind");
+  if ((kind == 1 || kind == 2) && n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
+  if (kind != 0 && !h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  Program pg = kind == 0   ? build_apply_A(h->op, h->pp)
+               : kind == 1 ? build_apply_M(h->op, n_it, h->pp)
+               : kind == 2 ? build_A_then_M(h->op, n_it, h->pp)
+                           : build_gs_sweep(h->op, h->pp);
+  const int64_t nt = (int64_t)pg.tasks.size();
+  *n_out = nt;
+  if (cap < nt) return fail(PT_EINVAL, "task record buffer too small");
+  for (int64_t q = 0; q < nt; ++q) {
+    const DevTask& t = pg.tasks[q];
+    int32_t* r = rec + PT_TASK_WORDS * q;
+    r[0] = t.type;
+    r[1] = t.signal;
+    r[2] = t.nwait;
+    r[3] = t.npiece;
+    r[4] = t.r0;
+    r[5] = t.r1;
+    r[6] = t.out.slot;
+    r[7] = (int32_t)t.out.off;
+    for (int i = 0; i < 8; ++i) {
+      const bool has = i < t.nwait;
+      r[8 + 2 * i] = has ? pg.waits[t.wait0 + i].ctr : -1;
+      r[9 + 2 * i] = has ? pg.waits[t.wait0 + i].val : 0;
+    }
+  }
   return 0;
 }
 

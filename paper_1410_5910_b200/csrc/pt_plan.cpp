@@ -58,6 +58,8 @@ class Builder {
   Builder(const Operator& op, const PlanParams& pp) : op_(op), pp_(pp) {}
   // pieces per T_PLR task for the blocks emitted next (0: pp.t_pieces)
   int t_pieces_now = 0;
+  // the blocks emitted next are on a sweep's dependency chain (queue priority)
+  bool chain_now = false;
   const PlanParams& params() const { return pp_; }
 
   int emit_block(VecRef out, const std::vector<TermSpec>& terms,
@@ -324,8 +326,11 @@ class Builder {
     for (size_t g = 0; g < groups_.size(); ++g)  // empty groups are complete at once
       if (gleft[g] == 0)
         for (int c : gcons_list[g]) --unmet[c];
+    // chain tasks first among the released ones: their latency is the
+    // launch's critical path, the rest fills in around them
+    auto prio = [&](int t) { return bl[t] + (task_chain_[t] ? pp_.chain_boost_us : 0.0); };
     for (int t = 0; t < n; ++t)
-      if (unmet[t] == 0) ready.push(PI(bl[t], -t));
+      if (unmet[t] == 0) ready.push(PI(prio(t), -t));
     std::vector<int> order;
     order.reserve(n);
     int busy = 0;
@@ -350,7 +355,7 @@ class Builder {
       const int g = task_group_[ev.second];
       if (--gleft[g] == 0)
         for (int c : gcons_list[g])
-          if (--unmet[c] == 0) ready.push(PI(bl[c], -c));
+          if (--unmet[c] == 0) ready.push(PI(prio(c), -c));
     }
     Program out;
     out.overflow = overflow_;
@@ -433,6 +438,7 @@ class Builder {
     task_waits_.push_back(waits);
     task_group_.push_back(g);
     task_cost_.push_back(cost);
+    task_chain_.push_back(chain_now);
   }
 
   const Operator& op_;
@@ -443,6 +449,7 @@ class Builder {
   std::vector<std::vector<int>> task_waits_;
   std::vector<int> task_group_;
   std::vector<double> task_cost_;
+  std::vector<bool> task_chain_;
   std::set<int64_t> sweep_kernels_;
   std::string overflow_;  // why the program cannot run (empty: it can)
 };
@@ -588,6 +595,7 @@ void emit_sweep(Builder& b, const Operator& op, VecRef rhs, bool has_uold, VecRe
   }
   // chain, level by level, both halves interleaved (small T tasks: a level's
   // t-phase spreads over all CTAs; its latency is on the critical path)
+  b.chain_now = true;
   for (int lv = 0; lv <= max_level; ++lv) {
     for (int h = 0; h < 2; ++h) {
       for (int64_t q = 0; q < nt; ++q) {
@@ -609,6 +617,7 @@ void emit_sweep(Builder& b, const Operator& op, VecRef rhs, bool has_uold, VecRe
     }
   }
   b.t_pieces_now = 0;
+  b.chain_now = false;
   b.end_stage();
 }
 

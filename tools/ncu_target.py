@@ -1,6 +1,6 @@
 """Launch one operator program a few times (ncu target; profiling aid).
 
-    python tools/ncu_target.py c3 A [reps]     # kinds: A, M, AM
+    python tools/ncu_target.py c3 A [reps] [max_iter]   # kinds: A, M, AM, G (GMRES)
 """
 import sys
 from pathlib import Path
@@ -24,6 +24,8 @@ for _ in range(reps):
         op.apply_A(x, out=y)
     elif kind == "M":
         op.apply_M(x, out=y)
+    elif kind == "AM":
+        op.apply_AM(x, out=y)
     else:
         op.gmres(torch.from_numpy(np.array(arr["rhs"][0])).cuda(), rel_tol=1e-9,
                  max_iter=int(sys.argv[4]) if len(sys.argv) > 4 else 2)
