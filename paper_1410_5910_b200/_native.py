@@ -75,6 +75,8 @@ _SIGS = {
     "pt_trace_program": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP, C.POINTER(C.c_int64),
                                    C.c_int64, C.POINTER(C.c_int64)]),
     "pt_plan_stats": (C.c_int, [_VP, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+    "pt_plan_tasks": (C.c_int, [_VP, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int64,
+                               C.POINTER(C.c_int64)]),
     "pt_exec_info": (C.c_int, [_VP, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64)]),
     "pt_last_error": (C.c_char_p, []),
