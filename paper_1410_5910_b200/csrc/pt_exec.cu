@@ -386,44 +386,50 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
 // in the per-piece barrier, per task
 __shared__ long long s_cyc_wait, s_cyc_sync;
 
+// the consumers' position in the ring (every consumer thread keeps a copy)
+struct Ring {
+  int stage;
+  uint32_t phase;
+};
+
 __device__ __forceinline__ const double2* wait_piece(const ExecArgs& a, const Layout& L,
-                                                     uint32_t seq, int q, int p) {
-  const uint32_t ns = (uint32_t)L.n_stages;
-  const int s = seq % ns;
+                                                     const Ring& rg, int q, int p) {
   const long long c0 = a.trace ? clock64() : 0;
-  bar_wait(&s_full[s], (seq / ns) & 1);
+  bar_wait(&s_full[rg.stage], rg.phase);
   if (a.trace && threadIdx.x == 0) {
     s_cyc_wait += clock64() - c0;
     if (p < 8) trace_mark(a, q, 6 + p);
   }
-  return L.stage(s);
+  return L.stage(rg.stage);
 }
 
-__device__ __forceinline__ void release_piece(const ExecArgs& a, const Layout& L, uint32_t& seq) {
-  const long long c0 = a.trace ? clock64() : 0;
-  consumer_sync();
-  if (threadIdx.x == 0) {
-    if (a.trace) s_cyc_sync += clock64() - c0;
-    bar_arrive(&s_empty[seq % (uint32_t)L.n_stages]);
+// each consumer warp releases the stage on its own (the stage's empty
+// barrier counts the 16 warps): no CTA-wide barrier per piece
+__device__ __forceinline__ void release_piece(const Layout& L, Ring& rg) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) bar_arrive(&s_empty[rg.stage]);
+  if (++rg.stage == L.n_stages) {
+    rg.stage = 0;
+    rg.phase ^= 1u;
   }
-  ++seq;
 }
 
 // T_PLR: t = scale * Vt (x_a [+ x_b]).  A group of L lanes (L = 8, 16 or 32
 // per piece, from the widest row) per Vt row: lane j sums columns j, j + L,
 // ... in order, then an xor tree over the group.
 __device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, const Slot& sl,
-                                          const Layout& L, uint32_t& seq, int q) {
+                                          const Layout& L, Ring& rg, int q) {
   double2* T = s_slot[SLOT_T];
   const double2 sc = sl.coef[0];
   const DevItem* items = sl.items();
   for (int p = 0; p < t.npiece; ++p) {
     const DevPiece& pc = sl.pieces()[p];
     const int lanes = pc.e0;
+    const int lsh = __ffs(lanes) - 1;  // lanes is 8, 16 or 32
     const int sub = threadIdx.x & (lanes - 1);
-    const double2* buf = wait_piece(a, L, seq, q, p);
-    for (int base = pc.f0; base < pc.f1; base += CONSUMERS / lanes) {
-      const int r = base + (int)threadIdx.x / lanes;
+    const double2* buf = wait_piece(a, L, rg, q, p);
+    for (int base = pc.f0; base < pc.f1; base += CONSUMERS >> lsh) {
+      const int r = base + (int)(threadIdx.x >> lsh);
       double2 acc = make_double2(0.0, 0.0);
       DevItem it{};
       if (r < pc.f1) {
@@ -438,7 +444,7 @@ __device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, c
       }
       if (r < pc.f1 && sub == 0) st_cg(T + t.tbase + r, cmul(sc, acc));
     }
-    release_piece(a, L, seq);
+    release_piece(L, rg);
   }
 }
 
@@ -459,19 +465,19 @@ __device__ __forceinline__ double2 epilogue_row(const DevTask& t, const Slot& sl
 // Y_PLR: one PLR_TILE-row tile; thread = (row r, column group g); columns
 // f = g (mod 16) ascending; the 16 group sums per row added in group order.
 __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, const Slot& sl,
-                                          const Layout& L, uint32_t& seq, int q) {
+                                          const Layout& L, Ring& rg, int q) {
   constexpr int G = CONSUMERS / PLR_TILE;
   const int r = threadIdx.x % PLR_TILE, g = threadIdx.x / PLR_TILE;
   const DevItem* items = sl.items();
   double2 acc = make_double2(0.0, 0.0);
   for (int p = 0; p < t.npiece; ++p) {
     const DevPiece& pc = sl.pieces()[p];
-    const double2* buf = wait_piece(a, L, seq, q, p);
+    const double2* buf = wait_piece(a, L, rg, q, p);
     for (int f = pc.f0 + ((g - pc.f0) % G + G) % G; f < pc.f1; f += G) {
       const DevItem it = items[f];
       if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
     }
-    release_piece(a, L, seq);
+    release_piece(L, rg);
   }
   double2* part = L.part();
   part[g * PLR_TILE + r] = acc;
@@ -487,14 +493,14 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
 // Y_DENSE: rows [r0, r1) (<= 4); piece p = rows of term p's kernel; columns
 // split over the 8 warps, per-warp scaled partials summed in warp order.
 __device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t, const Slot& sl,
-                                            const Layout& L, uint32_t& seq, int q) {
+                                            const Layout& L, Ring& rg, int q) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.m;
   const int nrows = t.r1 - t.r0;
   double2* part = L.part();
   if (lane < DENSE_RT_MAX) part[warp * DENSE_RT_MAX + lane] = make_double2(0.0, 0.0);
   for (int it = 0; it < t.nterm; ++it) {
-    const double2* K = wait_piece(a, L, seq, q, it);
+    const double2* K = wait_piece(a, L, rg, q, it);
     const double2* x = sl.vec + 2 * it * m;
     double2 d[DENSE_RT_MAX];
 #pragma unroll
@@ -512,7 +518,7 @@ __device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t,
       if (lane == i && i < nrows)
         part[warp * DENSE_RT_MAX + i] = cfma(sc, rr, part[warp * DENSE_RT_MAX + i]);
     }
-    release_piece(a, L, seq);
+    release_piece(L, rg);
   }
   consumer_sync();
   if ((int)threadIdx.x < nrows) {
@@ -523,7 +529,7 @@ __device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t,
 }
 
 __device__ void consumer(const ExecArgs& a, const Layout& L) {
-  uint32_t seq = 0;  // pieces consumed
+  Ring rg{0, 0u};  // pieces consumed
   for (int use = 0;; ++use) {
     const int k = use % EXEC_TSLOTS;
     const Slot sl = L.slot(k);
@@ -533,11 +539,11 @@ __device__ void consumer(const ExecArgs& a, const Layout& L) {
     const int q = t.q;
     if (threadIdx.x == 0) trace_mark(a, q, 4);
     if (t.type == TASK_T_PLR)
-      run_t_plr(a, t, sl, L, seq, q);
+      run_t_plr(a, t, sl, L, rg, q);
     else if (t.type == TASK_Y_PLR)
-      run_y_plr(a, t, sl, L, seq, q);
+      run_y_plr(a, t, sl, L, rg, q);
     else
-      run_y_dense(a, t, sl, L, seq, q);
+      run_y_dense(a, t, sl, L, rg, q);
     consumer_sync();
     if (threadIdx.x == 0) {  // the slot's producer warp publishes the outputs
       trace_mark(a, q, 2);
@@ -577,7 +583,7 @@ __global__ void __launch_bounds__(EXEC_THREADS, 1) pt_exec_kernel(ExecArgs a) {
     s_seq = 0;
     for (int i = 0; i < a.n_stages; ++i) {
       bar_init(&s_full[i], 1);
-      bar_init(&s_empty[i], 1);
+      bar_init(&s_empty[i], EXEC_CONSUMERS / 32);
     }
     for (int i = 0; i < EXEC_TSLOTS; ++i) {
       bar_init(&s_tfull[i], 1);
