@@ -137,6 +137,7 @@ struct pt_handle {
   int64_t blob_cap = 0;    // bytes of a task slot's metadata blob area
   int64_t slot_bytes = 0;  // bytes of one task slot
   int n_stages = 4;        // operator ring stages
+  int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
   std::unique_ptr<pt_gmres_ws> gws;
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
@@ -476,6 +477,7 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.src_cap = h->src_cap;
   a.slot_bytes = h->slot_bytes;
   a.n_stages = h->n_stages;
+  a.poll_ns = h->poll_ns;
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
   a.stop = stop;
@@ -791,6 +793,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_T_SLOTS")) h->pp.plr_slots_per_task = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_T_PIECES")) h->pp.t_pieces = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_ROW_CHUNK")) h->pp.row_chunk = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PT_POLL_NS")) h->poll_ns = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PT_CHAIN_BOOST")) h->pp.chain_boost_us = std::atof(e);
   if (const char* e = std::getenv("PT_SIM_SLOTS")) h->pp.ctas = h->grid * std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_TASK_US")) h->pp.task_us = std::atof(e);

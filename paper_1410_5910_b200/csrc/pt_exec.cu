@@ -45,8 +45,12 @@ __shared__ __align__(8) unsigned long long s_tempty[EXEC_TSLOTS];     // slot re
 __shared__ __align__(8) unsigned long long s_meta[EXEC_TSLOTS];       // blob landed (tx)
 __shared__ __align__(8) unsigned long long s_stg[EXEC_TSLOTS];        // vectors landed (tx)
 __shared__ volatile int s_grab_turn;     // slot use whose task may be grabbed next
-__shared__ volatile int s_issue_turn;    // slot use whose pieces may be issued
-__shared__ volatile uint32_t s_seq;      // operator pieces issued so far (ring position)
+// Ring positions are reserved per slot use, in use order, as soon as the
+// task's piece count is known: a use's pieces may then be issued before the
+// previous use has issued all of its own (each position waits only for the
+// stage's previous occupant to be consumed).
+__shared__ volatile int s_resv_turn;     // slot use that reserves positions next
+__shared__ volatile uint32_t s_next_pos; // first unreserved ring position
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -190,12 +194,11 @@ __device__ __forceinline__ void trace_mark(const ExecArgs& a, int q, int k) {
 
 // ---- producers (warps 8, 9) ---------------------------------------------------------
 
-// lane 0 of the warp holding the issue turn: piece p of the slot's task into
-// the ring stage of sequence number seq
+// lane 0: issue piece p of the slot's task into ring position pos
 __device__ __forceinline__ void issue_piece(const ExecArgs& a, const Layout& L, const Slot& sl,
-                                            int q, int p, uint32_t seq) {
+                                            int q, int p, uint32_t pos) {
   const DevPiece& pc = sl.pieces()[p];
-  const int s = seq % (uint32_t)L.n_stages;
+  const int s = pos % (uint32_t)L.n_stages;
   const uint32_t bytes = (uint32_t)pc.elems * (uint32_t)sizeof(double2);
   const double2* src = (sl.desc().type == TASK_Y_DENSE ? a.dense : a.fac) + pc.src;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -204,10 +207,11 @@ __device__ __forceinline__ void issue_piece(const ExecArgs& a, const Layout& L, 
   if (p < 8) trace_mark(a, q, 14 + p);
 }
 
-// lane 0: is the ring stage of sequence number seq free for its next use?
-__device__ __forceinline__ bool stage_free(const Layout& L, uint32_t seq) {
+// lane 0: is the stage of ring position pos free (its previous occupant,
+// position pos - n_stages, consumed)?
+__device__ __forceinline__ bool stage_free(const Layout& L, uint32_t pos) {
   const uint32_t ns = (uint32_t)L.n_stages;
-  return seq < ns || bar_test(&s_empty[seq % ns], ((seq / ns) - 1) & 1);
+  return pos < ns || bar_test(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
 }
 
 // Term scales, eye coefficients and the vector pointers the staging
@@ -321,6 +325,8 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     q = __shfl_sync(0xffffffffu, q, 0);
     if (q >= a.n_tasks) {  // end: consumers stop at the first empty slot use
       if (lane == 0) {
+        while (s_resv_turn != use) __nanosleep(16);
+        s_resv_turn = use + 1;
         reinterpret_cast<DevTask*>(sl.blob)->type = -1;
         bar_arrive(&s_tfull[k]);
       }
@@ -338,12 +344,17 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     const DevTask& t = sl.desc();
     parse_meta(t, sl, lane);
     int issued = 0;
+    uint32_t pos0 = 0;  // the use's first ring position
     if (lane == 0) {
-      if (s_issue_turn == use) {  // our turn on the ring: pieces before the wait
-        __threadfence_block();
-        uint32_t seq = s_seq;
-        while (issued < t.npiece && stage_free(L, seq)) issue_piece(a, L, sl, q, issued++, seq++);
-        s_seq = seq;
+      while (s_resv_turn != use) __nanosleep(16);
+      pos0 = s_next_pos;
+      s_next_pos = pos0 + (uint32_t)t.npiece;
+      __threadfence_block();
+      s_resv_turn = use + 1;
+      // pieces before the dependency wait, into stages already free
+      while (issued < t.npiece && stage_free(L, pos0 + issued)) {
+        issue_piece(a, L, sl, q, issued, pos0 + issued);
+        ++issued;
       }
     }
     {  // dependencies: the lanes poll the task's counters in parallel
@@ -354,7 +365,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
         for (int i = lane; i < t.nwait; i += 32)
           if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
         ok = __all_sync(0xffffffffu, ok);
-        if (!ok) __nanosleep(20);
+        if (!ok && a.poll_ns > 0) __nanosleep(a.poll_ns);
       } while (!ok);
     }
     if (lane == 0) trace_mark(a, q, 1);
@@ -364,17 +375,12 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     if (lane == 0) {
       trace_mark(a, q, 5);
       bar_arrive(&s_tfull[k]);  // release: blob, vectors, epilogue visible to consumers
-      // the rest of the task's pieces, in ring order after the previous use's
-      while (s_issue_turn != use) __nanosleep(32);
-      __threadfence_block();
-      uint32_t seq = s_seq;
-      while (issued < t.npiece) {
-        if (seq >= ns) bar_wait(&s_empty[seq % ns], ((seq / ns) - 1) & 1);
-        issue_piece(a, L, sl, q, issued++, seq++);
+      // the rest of the task's pieces, as their stages free up
+      for (; issued < t.npiece; ++issued) {
+        const uint32_t pos = pos0 + issued;
+        if (pos >= ns) bar_wait(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
+        issue_piece(a, L, sl, q, issued, pos);
       }
-      s_seq = seq;
-      __threadfence_block();
-      s_issue_turn = use + 1;
     }
     __syncwarp();
   }
@@ -578,9 +584,9 @@ __global__ void __launch_bounds__(EXEC_THREADS, 1) pt_exec_kernel(ExecArgs a) {
   }
   if (threadIdx.x == 0) {
     s_cyc_wait = s_cyc_sync = 0;
-    s_issue_turn = 0;
+    s_resv_turn = 0;
     s_grab_turn = 0;
-    s_seq = 0;
+    s_next_pos = 0;
     for (int i = 0; i < a.n_stages; ++i) {
       bar_init(&s_full[i], 1);
       bar_init(&s_empty[i], EXEC_CONSUMERS / 32);
