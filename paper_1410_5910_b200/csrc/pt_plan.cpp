@@ -61,6 +61,12 @@ class Builder {
   // the blocks emitted next are on a sweep's dependency chain (queue priority)
   bool chain_now = false;
   const PlanParams& params() const { return pp_; }
+  // operator elements per T_PLR piece for the blocks emitted next (smaller
+  // on the sweep chain: a chain task's compute is on the critical path)
+  int64_t t_piece_cap() const {
+    return chain_now && pp_.chain_piece_elems > 0 ? std::min(pp_.half_elems, pp_.chain_piece_elems)
+                                                  : pp_.half_elems;
+  }
 
   int emit_block(VecRef out, const std::vector<TermSpec>& terms,
                  const std::vector<EyeSpec>& eyes, bool has_init, VecRef init,
@@ -112,7 +118,7 @@ class Builder {
             while (s1 < ns && s1 - s0 < cap) {
               const DevSlot& sl = op_.slots[kp.slot0 + s1];
               const int64_t c = sl.cols;
-              if (s1 - s0 > pc.f0 && elems + c > pp_.half_elems) break;
+              if (s1 - s0 > pc.f0 && elems + c > t_piece_cap()) break;
               // the staged source slice [c0, c1) of the task stays within tcols_cap
               const int32_t lo = std::min(span0, sl.col_off);
               const int32_t hi = std::max(span1, sl.col_off + sl.cols);

@@ -71,6 +71,7 @@ struct PlanParams {
   int t_pieces_chain = 1;        // ... in the sweeps' dependency chain
   int row_chunk = ROW_CHUNK;     // output rows published per producer group
   double chain_boost_us = 0.0;   // queue priority bonus of sweep-chain tasks
+  int64_t chain_piece_elems = 0; // T_PLR piece cap on the sweep chain (0: a stage)
   int64_t item_cap = 1 << 20;    // metadata items a task slot holds
   int64_t tcols_cap = MAX_TCOLS; // source columns a T_PLR task stages
 };
