@@ -90,7 +90,7 @@ def workload_config(name, meta, extra=None):
         "kernel_format": meta.get("kernel_format"),
         "kernel_bytes": meta.get("kernel_bytes"),
         "gmres_tol": meta["gmres_tol"], "max_iter": meta["gmres_max_iter"], "n_it": meta["n_it"],
-        "rhs": meta["solves"][0]["label"],
+        "rhs": meta["solves"][0]["label"] if meta.get("solves") else "rhs[0] (point source)",
         "l2": "flushed between steps (256 MiB write); operator %.0f MB vs 126 MB L2"
               % (meta.get("kernel_bytes", 0) / 1e6),
         "parallelism": "replicas",
@@ -209,7 +209,8 @@ def run_reference(args):
     name, path = pick_case(args.config)
     from paper_1410_5910_b200.operator import load_case_arrays
     meta, arr = load_case_arrays(path)
-    k_full = meta["solves"][0]["iterations"]
+    # reference iteration count (no reference solve recorded, e.g. c4: ours)
+    k_full = meta["solves"][0]["iterations"] if meta.get("solves") else meta.get("our_iterations", 12)
     budget = min(args.cpu_budget, 150.0 / max(args.steps + args.warmup, 1))
     for _ in range(args.warmup):
         cpu_sample(meta, arr, budget, k_full)
@@ -347,8 +348,11 @@ def run_ours(args):
     b_chk = torch.from_numpy(np.array(arr["rhs"][ri])).to(f"cuda:{local}")
     x_chk, rep_chk = op.gmres(b_chk, rel_tol=tol, max_iter=max_iter, n_it=n_it)
     xs = x_chk.cpu().numpy() if hasattr(x_chk, "cpu") else np.asarray(x_chk)
-    ref_tr = np.asarray(arr["ref_traces"][0])
-    trace_err = float(np.linalg.norm(xs[:nt * m] + xs[nt * m:] - ref_tr) / np.linalg.norm(ref_tr))
+    if "ref_traces" in arr:
+        ref_tr = np.asarray(arr["ref_traces"][0])
+        trace_err = float(np.linalg.norm(xs[:nt * m] + xs[nt * m:] - ref_tr) / np.linalg.norm(ref_tr))
+    else:  # no reference solve for this case (c4: see DESIGN.md, parity vs the oracle)
+        trace_err = None
     k = rep_chk["iterations"]
 
     if rank != 0:
@@ -368,7 +372,8 @@ def run_ours(args):
         "data": "synthetic (seeded medium per SURVEY.md §8(d); operator from the reference's "
                 "offline stage, cached)",
         "config": workload_config(name, meta, {"iterations": k,
-                                               "reference_iterations": meta["solves"][0]["iterations"],
+                                               "reference_iterations": (meta["solves"][0]["iterations"]
+                                                                        if meta.get("solves") else None),
                                                "trace_rel_err_vs_reference": trace_err}),
         "impl": "ours",
         "roofline": {
