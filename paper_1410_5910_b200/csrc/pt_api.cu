@@ -115,6 +115,7 @@ struct pt_gmres_ws {
 struct pt_handle {
   int device = 0;
   bool host_only = false;  // PT_DEVICE_HOST: plan tables only
+  bool dense_leaves = true;  // store factor-heavy PLR leaves as U.Vt (PT_DENSE_LEAVES=0: off)
   Operator op;
   std::string sweep_err;
   PlanParams pp;
@@ -241,9 +242,14 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
     std::vector<const pt_leaf*> kl;
     for (; pos < idx.size() && leaves[idx[pos]].kernel == k; ++pos) {
       const pt_leaf& L = leaves[idx[pos]];
-      op.kernel_bytes[k] += 16 * L.rank * (L.rows + L.cols);
+      op.kernel_bytes[k] += 16 * L.rank * (L.rows + L.cols);  // the reference's bytes
       if (L.rank > 0) kl.push_back(&L);
     }
+    // leaves whose factors outweigh their product are stored as the product
+    // U.Vt (FP64, the same matrix to rounding): fewer bytes, and no T work
+    auto dense_leaf = [&](const pt_leaf* L) {
+      return h->dense_leaves && L->rank * (L->rows + L->cols) > L->rows * L->cols;
+    };
     // slots ordered by column band: a T task's run of slots then reads a
     // narrow range of the source vector
     std::stable_sort(kl.begin(), kl.end(), [](const pt_leaf* a, const pt_leaf* b) {
@@ -261,6 +267,11 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
       dl.rank = (int32_t)L->rank;
       dl.slot0 = slot;
       dl.v_off = (int64_t)blob.size();
+      if (dense_leaf(L)) {  // no Vt rows: the leaf's columns act as its "rank" columns
+        dl.slot0 = -1;
+        op.leaves.push_back(dl);
+        continue;
+      }
       const double* Vt = fac + 2 * L->vt_off;
       for (int64_t c = 0; c < L->rank; ++c) {
         DevSlot sl{};
@@ -297,8 +308,25 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
         te.rank = dl.rank;
         te.lo = (int16_t)(r_first - lo);
         te.hi = (int16_t)(r_end - lo);
-        for (int64_t c = 0; c < L.rank; ++c)
-          for (int64_t r = r_first; r < r_end; ++r) blob.push_back(U(L, r - dl.row_off, c));
+        if (dl.slot0 < 0) {  // dense leaf: the tile's rows of U.Vt, column by column
+          te.rank = dl.cols;
+          te.pre = dl.col_off;
+          const double* Vt = fac + 2 * L.vt_off;
+          for (int64_t c = 0; c < L.cols; ++c)
+            for (int64_t r = r_first; r < r_end; ++r) {
+              double re = 0.0, im = 0.0;
+              for (int64_t j = 0; j < L.rank; ++j) {
+                const double2 u = U(L, r - dl.row_off, j);
+                const double vr = Vt[2 * (j * L.cols + c)], vi = Vt[2 * (j * L.cols + c) + 1];
+                re = std::fma(u.x, vr, std::fma(-u.y, vi, re));
+                im = std::fma(u.x, vi, std::fma(u.y, vr, im));
+              }
+              blob.push_back(make_double2(re, im));
+            }
+        } else {
+          for (int64_t c = 0; c < L.rank; ++c)
+            for (int64_t r = r_first; r < r_end; ++r) blob.push_back(U(L, r - dl.row_off, c));
+        }
         op.tile_ent.push_back(te);
       }
     }
@@ -330,15 +358,16 @@ int ensure_slot(pt_handle* h, int s, int64_t elems) {
 // Per-task metadata blobs, in queue order, so a producer warp fetches a
 // task's whole description with one bulk copy:
 //   [DevTask][DevPiece x npiece][DevTerm x nterm][DevEye x neye]
-//   [DevWait x nwait][DevRun x nrun][DevItem x nitem]
+//   [DevWait x nwait][DevRun x nrun][DevSrcRun x nsrun][DevItem x nitem]
 // each section 16-byte aligned.  In the blob copy of the DevTask, piece0 /
-// term0 / eye0 / wait0 / run0 / item0 are byte offsets of the sections and
+// term0 / eye0 / wait0 / run0 / srun0 / item0 are byte offsets of the sections and
 // q is the queue index.
 int64_t blob_bytes_max(int64_t item_cap) {
   auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
   return al(sizeof(DevTask)) + al(EXEC_PIECES * sizeof(DevPiece)) + al(EXEC_TERMS * sizeof(DevTerm)) +
          al(EXEC_EYES * sizeof(DevEye)) + al(EXEC_WAITS * sizeof(DevWait)) +
-         al(EXEC_RUNS * sizeof(DevRun)) + al(item_cap * (int64_t)sizeof(DevItem));
+         al(EXEC_RUNS * sizeof(DevRun)) + al(EXEC_RUNS * sizeof(DevSrcRun)) +
+         al(item_cap * (int64_t)sizeof(DevItem));
 }
 
 void build_blobs(const Program& pg, std::vector<int4>& blob, std::vector<int64_t>& off,
@@ -362,6 +391,7 @@ void build_blobs(const Program& pg, std::vector<int4>& blob, std::vector<int64_t
     d.eye0 = put(pg.eyes.data() + t.eye0, (size_t)t.neye * sizeof(DevEye));
     d.wait0 = put(pg.waits.data() + t.wait0, (size_t)t.nwait * sizeof(DevWait));
     d.run0 = put(pg.runs.data() + t.run0, (size_t)t.nrun * sizeof(DevRun));
+    d.srun0 = put(pg.sruns.data() + t.srun0, (size_t)t.nsrun * sizeof(DevSrcRun));
     d.item0 = put(pg.items.data() + t.item0, (size_t)t.nitem * sizeof(DevItem));
     d.q = (int32_t)q;
     std::memcpy(b.data(), &d, sizeof(DevTask));
@@ -379,12 +409,12 @@ int check_slots(const pt_handle* h, const Program& pg) {
   for (const DevTask& t : pg.tasks) {  // what one task slot stages
     int64_t vec = 0;
     if (t.type == TASK_T_PLR) vec = 2 * (t.c1 - t.c0);  // both sources of a merged term
-    if (t.type == TASK_Y_PLR) vec = t.nitem;
+    if (t.type == TASK_Y_PLR) vec = t.nitem + t.ndense2;
     if (t.type == TASK_Y_DENSE) vec = 2 * (int64_t)t.nterm * h->op.m;
     const int rows = t.type == TASK_Y_DENSE ? DENSE_RT_MAX : EXEC_EPI;
     if (vec > h->src_cap || t.nitem > h->item_cap || t.nterm > EXEC_TERMS ||
         t.neye > EXEC_EYES || t.npiece > EXEC_PIECES || t.nwait > EXEC_WAITS ||
-        t.nrun > EXEC_RUNS ||
+        t.nrun > EXEC_RUNS || t.nsrun > EXEC_RUNS ||
         (t.type != TASK_T_PLR && t.r1 - t.r0 > rows))
       return fail(PT_EINVAL, "a task stages more than the executor's task slot holds");
   }
@@ -648,6 +678,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   std::unique_ptr<pt_handle> h(new pt_handle());
   h->device = device;
   h->host_only = host_only;
+  if (const char* e = std::getenv("PT_DENSE_LEAVES")) h->dense_leaves = std::atoi(e) != 0;
   Operator& op = h->op;
   op.m = layout->m;
   op.nb = layout->n_block_rows;
@@ -693,17 +724,20 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     // item per Vt row (<= MAX_T_SLOTS) and a source slice (<= tcols_cap)
     PlanParams probe;
     probe.half_elems = (int64_t)1 << 30;
-    int64_t ycols = 0;
+    int64_t ycols = 0, yvec = 0;
     for (const Program& pg : {build_apply_A(op, probe), build_apply_M(op, 2, probe),
                               build_gs_sweep(op, probe)})
       for (const DevTask& t : pg.tasks)
-        if (t.type == TASK_Y_PLR) ycols = std::max<int64_t>(ycols, t.nitem);
+        if (t.type == TASK_Y_PLR) {
+          ycols = std::max<int64_t>(ycols, t.nitem);
+          yvec = std::max<int64_t>(yvec, t.nitem + t.ndense2);
+        }
     int64_t widest = 0;
     for (const DevSlot& sl : op.slots) widest = std::max<int64_t>(widest, sl.cols);
     h->item_cap = (std::max<int64_t>(ycols, MAX_T_SLOTS) + 7) / 8 * 8;
     h->pp.tcols_cap = std::max<int64_t>(widest, std::min<int64_t>(op.m, MAX_TCOLS));
     // Y: one t value per column; T: both sources of a merged term's slice
-    h->src_cap = std::max<int64_t>(h->item_cap, 2 * h->pp.tcols_cap);
+    h->src_cap = std::max<int64_t>(std::max<int64_t>(h->item_cap, yvec), 2 * h->pp.tcols_cap);
     h->pp.item_cap = h->item_cap;
   } else {
     // a dense Y task stages one source vector per kernel term: the most terms

@@ -138,6 +138,9 @@ struct Slot {
   __device__ __forceinline__ const DevRun* runs() const {
     return reinterpret_cast<const DevRun*>(blob + desc().run0);
   }
+  __device__ __forceinline__ const DevSrcRun* sruns() const {
+    return reinterpret_cast<const DevSrcRun*>(blob + desc().srun0);
+  }
 };
 
 // computed on use (arrays of pointers would be indexed dynamically and live
@@ -249,7 +252,7 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
   if (t.type == TASK_T_PLR) {
     bytes = (uint32_t)(t.c1 - t.c0) * (sl.src[1] ? 2u : 1u);
   } else if (t.type == TASK_Y_PLR) {
-    bytes = (uint32_t)t.nitem;
+    bytes = (uint32_t)(t.nitem + t.ndense2);
   } else {
     for (int it = 0; it < t.nterm; ++it) bytes += (uint32_t)m * (sl.src[2 * it + 1] ? 2u : 1u);
   }
@@ -275,6 +278,14 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
       const DevRun r = runs[i];
       bulk_copy(sl.vec + r.f, T + r.t, (uint32_t)r.n * (uint32_t)sizeof(double2), &s_stg[k]);
     }
+    const DevSrcRun* sr = sl.sruns();  // dense leaves: source columns (both sources)
+    for (int i = lane; i < t.nsrun; i += 32) {
+      const DevSrcRun r = sr[i];
+      const uint32_t nb = (uint32_t)r.n * (uint32_t)sizeof(double2);
+      bulk_copy(sl.vec + r.f, sl.src[2 * r.term] + r.col, nb, &s_stg[k]);
+      if (sl.src[2 * r.term + 1])
+        bulk_copy(sl.vec + t.nitem + r.b_off, sl.src[2 * r.term + 1] + r.col, nb, &s_stg[k]);
+    }
   } else {
     for (int i = lane; i < 2 * t.nterm; i += 32)
       if (const double2* src = sl.src[i])
@@ -290,6 +301,18 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
     if (sl.src[1]) {
       const int n = t.c1 - t.c0;
       for (int c = lane; c < n; c += 32) sl.vec[c] = cadd(sl.vec[c], sl.vec[n + c]);
+    }
+  } else if (t.type == TASK_Y_PLR) {  // dense-leaf columns: scale * (x_a + x_b)
+    const DevSrcRun* sr = sl.sruns();
+    for (int i = 0; i < t.nsrun; ++i) {
+      const DevSrcRun r = sr[i];
+      const double2 sc = sl.coef[r.term];
+      const bool two = sl.src[2 * r.term + 1] != nullptr;
+      for (int c = lane; c < r.n; c += 32) {
+        double2 v = sl.vec[r.f + c];
+        if (two) v = cadd(v, sl.vec[t.nitem + r.b_off + c]);
+        sl.vec[r.f + c] = cmul(sc, v);
+      }
     }
   } else if (t.type == TASK_Y_DENSE) {
     for (int it = 0; it < t.nterm; ++it)

@@ -200,6 +200,7 @@ class Builder {
     const int64_t chunk_rows = std::max<int64_t>(pp_.row_chunk / rpt, 1) * rpt;
     int g = -1;
     for (int64_t r0 = 0; r0 < m; r0 += rpt) {
+      std::vector<int> dense_waits;  // source rows the task's dense leaves read
       if (r0 % chunk_rows == 0) {
         g = new_group();
         register_producer_rows(out, r0, std::min<int64_t>(m, r0 + chunk_rows), g);
@@ -209,7 +210,8 @@ class Builder {
       if (plr) {  // one item per flat (leaf, rank column) of all terms, pieces of whole columns
         tk.item0 = (int32_t)prog_.items.size();
         tk.run0 = (int32_t)prog_.runs.size();
-        int32_t f = 0;
+        tk.srun0 = (int32_t)prog_.sruns.size();
+        int32_t f = 0, dense2 = 0;
         for (size_t it = 0; it < terms.size(); ++it) {
           const DevTerm& dt = prog_.terms[term0 + it];
           const int32_t k0 = op_.kplr[dt.kernel].tile0 + (int32_t)(r0 / PLR_TILE);
@@ -217,12 +219,23 @@ class Builder {
           bool open = false;
           for (int32_t e = op_.tile_ptr[k0]; e < op_.tile_ptr[k0 + 1]; ++e) {
             const DevTileEntry& te = op_.tile_ent[e];
-            if (te.rank > 0) {
+            if (te.rank > 0 && te.t0 >= 0) {  // t values from the term's T tasks
               DevRun run{};
               run.t = (int32_t)(dt.t_base + te.t0);
               run.f = (int16_t)f;
               run.n = (int16_t)te.rank;
               prog_.runs.push_back(run);
+            } else if (te.rank > 0) {  // dense leaf: scaled source columns
+              DevSrcRun sr{};
+              sr.col = te.pre;
+              sr.f = (int16_t)f;
+              sr.n = (int16_t)te.rank;
+              sr.term = (int16_t)it;
+              sr.b_off = (int16_t)dense2;
+              if (dt.nsrc > 1) dense2 += te.rank;
+              prog_.sruns.push_back(sr);
+              for (int sidx = 0; sidx < dt.nsrc; ++sidx)
+                add_wait_rows(dense_waits, dt.src[sidx], te.pre, te.pre + te.rank);
             }
             for (int32_t c = 0; c < te.rank; ++c, ++f) {
               const int64_t addr = te.u0 + (int64_t)c * te.stride;
@@ -250,6 +263,8 @@ class Builder {
         }
         tk.nitem = (int32_t)prog_.items.size() - tk.item0;
         tk.nrun = (int32_t)prog_.runs.size() - tk.run0;
+        tk.nsrun = (int32_t)prog_.sruns.size() - tk.srun0;
+        tk.ndense2 = dense2;
         tk.ncol = f;
         if (tk.nitem > pp_.item_cap) flag("a PLR row tile has more rank columns than a task slot holds");
       } else {
@@ -280,6 +295,8 @@ class Builder {
       tk.rhs = rhs;
       tk.rhs_coef = rhs_coef;
       std::vector<int> tw = waits;
+      for (int g2 : dense_waits)
+        if (std::find(tw.begin(), tw.end(), g2) == tw.end()) tw.push_back(g2);
       for (const EyeSpec& e : eyes) add_wait_rows(tw, e.src, tk.r0, tk.r1);
       if (has_init) add_wait_rows(tw, init, tk.r0, tk.r1);
       if (has_rhs) add_wait_rows(tw, rhs, tk.r0, tk.r1);
@@ -371,6 +388,7 @@ class Builder {
     out.pieces = prog_.pieces;
     out.items = prog_.items;
     out.runs = prog_.runs;
+    out.sruns = prog_.sruns;
     out.t_elems = prog_.t_elems;
     out.term_bytes = prog_.term_bytes;
     out.algo_bytes = prog_.algo_bytes;

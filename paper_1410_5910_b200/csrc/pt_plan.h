@@ -44,6 +44,7 @@ struct Program {
   std::vector<DevPiece> pieces;    // staged operator ranges of every task
   std::vector<DevItem> items;      // per-task metadata items
   std::vector<DevRun> runs;        // Y_PLR t-value runs
+  std::vector<DevSrcRun> sruns;    // Y_PLR dense-leaf source runs
   int n_counters = 0;
   int64_t t_elems = 0;      // size of SLOT_T needed
   int64_t term_bytes = 0;   // kernel bytes actually streamed by the terms

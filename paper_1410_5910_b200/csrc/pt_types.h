@@ -89,7 +89,8 @@ struct DevTask {
   int32_t c0, c1;          // T_PLR: source columns [c0, c1) its Vt rows read
   int32_t tbase;           // T_PLR: SLOT_T index of the task's first Vt row
   int32_t q;               // queue index (set in the executor's metadata blob)
-  int32_t pad[3];
+  int32_t srun0, nsrun;    // Y_PLR: runs of dense-leaf source columns
+  int32_t ndense2;         // Y_PLR: second-source values those runs stage
 };
 
 // Per-task metadata item, 8 bytes, precomputed on the host.
@@ -110,6 +111,18 @@ struct DevRun {
   int32_t t;
   int16_t f;
   int16_t n;
+};
+
+// Y_PLR, dense leaf (a leaf whose U.Vt is stored as its product): the flat
+// columns [f, f + n) take scale * (x_a + x_b) of source columns [col, col + n)
+// of term `term`; x_b lands at staged offset nitem + b_off first
+struct DevSrcRun {
+  int32_t col;
+  int16_t f;
+  int16_t n;
+  int16_t term;
+  int16_t b_off;
+  int32_t pad;
 };
 
 // PLR storage on the device.  For each leaf the factors are stored as
@@ -144,13 +157,15 @@ struct DevKernelPLR {
 // each tile, each leaf meeting it, each rank column, the tile's rows of that
 // column (hi - lo values).  Tile row r (lo <= r < hi) of column c is at
 // u0 + c*stride + (r - lo), stride = hi - lo, u0 an absolute factor offset.
+// A dense leaf (t0 = -1: one whose factors hold more bytes than U.Vt itself,
+// e.g. the full-rank near-diagonal leaves) stores the tile's rows of U.Vt
+// instead, its "rank" columns being the leaf's columns (rank = cols).
 struct DevTileEntry {
   int64_t u0;
-  int32_t t0;      // first slot of the leaf (kernel-relative in the operator table,
-                   // absolute SLOT_T index in a program's task entries)
+  int32_t t0;      // first slot of the leaf (kernel-relative; -1: dense leaf)
   int32_t stride;  // leaf rows (U is column-major)
   int32_t rank;
-  int32_t pre;     // task entries: columns of the preceding entries of the task
+  int32_t pre;     // dense leaf (t0 < 0): its first column in the block
   int16_t lo, hi;
   int32_t pad;
 };

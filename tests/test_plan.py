@@ -4,8 +4,10 @@ The plan builder is the executor's compiler: it splits every operator apply
 into dataflow tasks, stages the operator in ring pieces and sizes the task
 slots.  These checks hold for any operator:
 - every program kind plans, and its task types add up;
-- the operator pieces stream exactly the algorithmic bytes once (each
-  kernel of an A-apply once; each D/R kernel of a sweep once per sweep);
+- the operator pieces stream the algorithmic bytes once (each kernel of an
+  A-apply once; each D/R kernel of a sweep once per sweep) -- exactly for
+  dense kernels, and fewer for PLR kernels whose factor-heavy leaves are
+  stored as their product U.Vt;
 - per-task metadata stays within the executor's slot limits;
 - a plan-only handle refuses device work with PT_EINVAL.
 """
@@ -46,7 +48,10 @@ def test_every_program_plans(name):
 def test_pieces_stream_the_algorithmic_bytes(name):
     op = host_op(name)
     a = op.plan_stats("A")
-    assert a["staged_bytes"] == a["algo_bytes"] > 0
+    if op.kernel_format == "dense":
+        assert a["staged_bytes"] == a["algo_bytes"] > 0
+    else:
+        assert 0 < a["staged_bytes"] <= a["algo_bytes"]
     m1 = op.plan_stats("M", 1)
     m2 = op.plan_stats("M", 2)
     # the second sweep re-reads every D/R kernel once more
@@ -62,6 +67,19 @@ def test_task_metadata_within_slot_limits(name):
         st = op.plan_stats(kind, 2)
         assert st["max_terms"] <= 16
         assert st["max_pieces"] <= 48
+
+
+def test_dense_leaves_only_remove_bytes(monkeypatch):
+    """Storing factor-heavy leaves as U.Vt changes the bytes, not the structure."""
+    name = next((f for f in FIXTURES if "plr" in f), None)
+    if name is None:
+        pytest.skip("no PLR fixture")
+    on = host_op(name).plan_stats("A")
+    monkeypatch.setenv("PT_DENSE_LEAVES", "0")
+    off = host_op(name).plan_stats("A")
+    assert off["staged_bytes"] == off["algo_bytes"] == on["algo_bytes"]
+    assert on["staged_bytes"] <= off["staged_bytes"]
+    assert on["y_plr"] == off["y_plr"] and on["t_plr"] <= off["t_plr"]
 
 
 def test_plan_only_handle_refuses_device_work():
@@ -80,4 +98,6 @@ def test_large_case_plans(name):
     """Reference-scale operators (when cases/ holds them) plan within limits."""
     op = host_op(name)
     st = op.plan_stats("AM", 2)
-    assert st["staged_bytes"] == op.plan_stats("A")["algo_bytes"] + op.plan_stats("M", 2)["algo_bytes"]
+    a, m2 = op.plan_stats("A"), op.plan_stats("M", 2)
+    assert st["staged_bytes"] == a["staged_bytes"] + m2["staged_bytes"]
+    assert st["staged_bytes"] <= a["algo_bytes"] + m2["algo_bytes"]
