@@ -136,6 +136,8 @@ struct pt_handle {
   int64_t src_cap = 0;     // complex elements of a task slot's vector staging
   int64_t item_cap = 0;    // items of a task slot
   int64_t blob_cap = 0;    // bytes of a task slot's metadata blob area
+  int64_t run_cap = 0;     // t-value runs of a task (PLR)
+  int64_t srun_cap = 0;    // dense-leaf source runs of a task (PLR)
   int64_t slot_bytes = 0;  // bytes of one task slot
   int n_stages = 4;        // operator ring stages
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
@@ -362,11 +364,11 @@ int ensure_slot(pt_handle* h, int s, int64_t elems) {
 // each section 16-byte aligned.  In the blob copy of the DevTask, piece0 /
 // term0 / eye0 / wait0 / run0 / srun0 / item0 are byte offsets of the sections and
 // q is the queue index.
-int64_t blob_bytes_max(int64_t item_cap) {
+int64_t blob_bytes_max(int64_t item_cap, int64_t run_cap, int64_t srun_cap) {
   auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
   return al(sizeof(DevTask)) + al(EXEC_PIECES * sizeof(DevPiece)) + al(EXEC_TERMS * sizeof(DevTerm)) +
          al(EXEC_EYES * sizeof(DevEye)) + al(EXEC_WAITS * sizeof(DevWait)) +
-         al(EXEC_RUNS * sizeof(DevRun)) + al(EXEC_RUNS * sizeof(DevSrcRun)) +
+         al(run_cap * (int64_t)sizeof(DevRun)) + al(srun_cap * (int64_t)sizeof(DevSrcRun)) +
          al(item_cap * (int64_t)sizeof(DevItem));
 }
 
@@ -414,7 +416,7 @@ int check_slots(const pt_handle* h, const Program& pg) {
     const int rows = t.type == TASK_Y_DENSE ? DENSE_RT_MAX : EXEC_EPI;
     if (vec > h->src_cap || t.nitem > h->item_cap || t.nterm > EXEC_TERMS ||
         t.neye > EXEC_EYES || t.npiece > EXEC_PIECES || t.nwait > EXEC_WAITS ||
-        t.nrun > EXEC_RUNS || t.nsrun > EXEC_RUNS ||
+        t.nrun > h->run_cap || t.nsrun > h->srun_cap ||
         (t.type != TASK_T_PLR && t.r1 - t.r0 > rows))
       return fail(PT_EINVAL, "a task stages more than the executor's task slot holds");
   }
@@ -731,6 +733,8 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
         if (t.type == TASK_Y_PLR) {
           ycols = std::max<int64_t>(ycols, t.nitem);
           yvec = std::max<int64_t>(yvec, t.nitem + t.ndense2);
+          h->run_cap = std::max<int64_t>(h->run_cap, t.nrun);
+          h->srun_cap = std::max<int64_t>(h->srun_cap, t.nsrun);
         }
     int64_t widest = 0;
     for (const DevSlot& sl : op.slots) widest = std::max<int64_t>(widest, sl.cols);
@@ -753,7 +757,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     h->src_cap = 2 * terms * op.m;  // both sources of every term
     h->item_cap = 0;
   }
-  h->blob_cap = (blob_bytes_max(h->item_cap) + 127) / 128 * 128;
+  h->blob_cap = (blob_bytes_max(h->item_cap, h->run_cap, h->srun_cap) + 127) / 128 * 128;
   h->slot_bytes =
       h->blob_cap +
       (h->src_cap + EXEC_EPI * EXEC_EPI_SRC + EXEC_TERMS + EXEC_EYES) * (int64_t)sizeof(double2) +

@@ -24,7 +24,6 @@ constexpr int EXEC_TRACE = 24;      // u64 trace words per task (pt_trace_progra
 constexpr int EXEC_PIECES = 48;     // operator pieces of one task (descriptors in the slot)
 constexpr int EXEC_SRCS = 2 * EXEC_TERMS + EXEC_EPI_SRC;  // vector pointers of one task
 constexpr int EXEC_WAITS = 64;      // dependency counters of one task (polled by 32 lanes)
-constexpr int EXEC_RUNS = 256;      // t-value runs of one Y_PLR task
 constexpr int DENSE_RT_MAX = 4;   // max rows of a Y_DENSE task (split-K over warps)
 constexpr int DENSE_ROWS_PER_TASK = 4;
 

@@ -18,6 +18,7 @@
 // ahead of its convergence check without changing the result.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 
@@ -228,25 +229,26 @@ __device__ void arn_reduce(const double2* P, int ldp, int nblk, int nc, double2*
 }
 
 // P[blockIdx.x, c] = sum_{e in slice} conj(V_c[e]) w[e]; warp per column,
-// the block's slice of w in shared memory
-__device__ void arn_dots(const double2* V, int64_t ldv, int nc, const double2* ws, int64_t lo,
-                         int len, double2* Prow) {
+// the block's slice of w in shared memory; Vb = element 0 of the slice of
+// column 0, columns ldb apart (global memory, or the slice staged in smem)
+__device__ void arn_dots(const double2* Vb, int64_t ldb, int nc, const double2* ws, int len,
+                         double2* Prow) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c = warp; c < nc; c += ARN_THREADS / 32) {
-    const double2* v = V + (int64_t)c * ldv + lo;
+    const double2* v = Vb + (int64_t)c * ldb;
     double2 acc = make_double2(0.0, 0.0);
-    for (int e = lane; e < len; e += 32) acc = cfma_conj(ld_cg(v + e), ws[e], acc);
+    for (int e = lane; e < len; e += 32) acc = cfma_conj(v[e], ws[e], acc);  // generic: smem or global
     acc = warp_sum(acc);
     if (lane == 0) st_cg(Prow + c, acc);
   }
 }
 
 // ws[e] -= sum_c V_c[e] h[c] over the block's slice (thread per element)
-__device__ void arn_update(const double2* V, int64_t ldv, int nc, const double2* h, double2* ws,
-                           int64_t lo, int len) {
+__device__ void arn_update(const double2* Vb, int64_t ldb, int nc, const double2* h, double2* ws,
+                           int len) {
   for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
     double2 acc = make_double2(0.0, 0.0);
-    for (int c = 0; c < nc; ++c) acc = cfma(ld_cg(V + (int64_t)c * ldv + lo + e), h[c], acc);
+    for (int c = 0; c < nc; ++c) acc = cfma(Vb[(int64_t)c * ldb + e], h[c], acc);
     ws[e] = csub(ws[e], acc);
   }
 }
@@ -266,12 +268,39 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
   const int len = (int)(lo + chunk < g.n ? chunk : (lo < g.n ? g.n - lo : 0));
   double2* hsm = sm;                  // coefficients (ldp)
   double2* ws = sm + g.ldp;           // the block's slice of w
+  double2* vs = ws + chunk;           // the block's slice of V[:, 0..j] (when it fits)
   double2* w = g.V + (int64_t)(j + 1) * g.n;
   double2* P1 = g.P;
   double2* P2 = g.P + (int64_t)RED_BLOCKS * g.ldp;
   __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
+  __shared__ __align__(8) unsigned long long s_vbar;
+  // the four passes over V read the block's slice once from HBM: staged in
+  // shared memory with TMA bulk copies (one per column) when it fits
+  const bool staged = (int64_t)nc * len <= g.arn_vcap && len > 0;
+  const double2* Vb = staged ? vs : g.V + lo;
+  const int64_t ldb = staged ? len : g.n;
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    if (staged) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&s_vbar))
+                   : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&s_vbar)),
+                   "r"((uint32_t)(nc * len * sizeof(double2)))
+                   : "memory");
+    }
+  }
   __syncthreads();
+  if (staged)
+    for (int c = threadIdx.x; c < nc; c += ARN_THREADS)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"((uint32_t)__cvta_generic_to_shared(vs + (int64_t)c * len)),
+          "l"(g.V + (int64_t)c * g.n + lo), "r"((uint32_t)(len * sizeof(double2))),
+          "r"((uint32_t)__cvta_generic_to_shared(&s_vbar))
+          : "memory");
   int bad = 0;
   for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
     const double2 v = ld_cg(w + lo + e);
@@ -281,8 +310,18 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
   if (bad) atomicOr(&s_bad, 1);
   __syncthreads();
   if (s_bad && threadIdx.x == 0) atomicOr(g.nonfinite, 1);
+  if (staged) {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+          " selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done)
+          : "r"((uint32_t)__cvta_generic_to_shared(&s_vbar))
+          : "memory");
+  }
   // pass 1: h1 = V^H w
-  arn_dots(g.V, g.n, nc, ws, lo, len, P1 + (int64_t)blockIdx.x * g.ldp);
+  arn_dots(Vb, ldb, nc, ws, len, P1 + (int64_t)blockIdx.x * g.ldp);
   grid.sync();
   arn_reduce(P1, g.ldp, nblk, nc, hsm);
   __syncthreads();
@@ -290,9 +329,9 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
     for (int c = threadIdx.x; c < nc; c += ARN_THREADS) st_cg(g.h1 + c, hsm[c]);
   __syncthreads();
   // pass 2: w -= V h1, h2 = V^H w
-  arn_update(g.V, g.n, nc, hsm, ws, lo, len);
+  arn_update(Vb, ldb, nc, hsm, ws, len);
   __syncthreads();
-  arn_dots(g.V, g.n, nc, ws, lo, len, P2 + (int64_t)blockIdx.x * g.ldp);
+  arn_dots(Vb, ldb, nc, ws, len, P2 + (int64_t)blockIdx.x * g.ldp);
   grid.sync();
   arn_reduce(P2, g.ldp, nblk, nc, hsm);
   __syncthreads();
@@ -300,7 +339,7 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
     for (int c = threadIdx.x; c < nc; c += ARN_THREADS) st_cg(g.h2 + c, hsm[c]);
   __syncthreads();
   // w -= V h2, ||w||^2
-  arn_update(g.V, g.n, nc, hsm, ws, lo, len);
+  arn_update(Vb, ldb, nc, hsm, ws, len);
   {
     double2 acc = make_double2(0.0, 0.0);
     for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
@@ -541,7 +580,7 @@ int grid_for(int64_t n) {
 cudaError_t gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
                             cudaGraphConditionalHandle cond, cudaStream_t s) {
   const int64_t chunk = (g.n + g.arn_blocks - 1) / g.arn_blocks;
-  const size_t smem = (size_t)(g.ldp + chunk) * sizeof(double2);
+  const size_t smem = (size_t)(g.ldp + chunk + g.arn_vcap) * sizeof(double2);
   count_launch();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.arn_blocks);
@@ -562,7 +601,12 @@ cudaError_t gm_arnoldi_setup(GmresDev& g, int device) {
   if (e != cudaSuccess) return e;
   g.arn_blocks = nsm < ARN_MAX_BLOCKS ? nsm : ARN_MAX_BLOCKS;
   const int64_t chunk = (g.n + g.arn_blocks - 1) / g.arn_blocks;
-  const size_t smem = (size_t)(g.ldp + chunk) * sizeof(double2);
+  int maxdyn = 0;
+  e = cudaDeviceGetAttribute(&maxdyn, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  const int64_t fixed = (int64_t)(g.ldp + chunk) * (int64_t)sizeof(double2);
+  g.arn_vcap = std::max<int64_t>(0, (maxdyn - 1024 - fixed) / (int64_t)sizeof(double2));
+  const size_t smem = (size_t)fixed + (size_t)g.arn_vcap * sizeof(double2);
   // per-function attribute shared by every workspace: it only grows
   static std::atomic<int> attr_max{0};
   int cur = attr_max.load();

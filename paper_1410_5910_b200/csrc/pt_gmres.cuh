@@ -36,6 +36,7 @@ struct GmresDev {
   int max_iter;
   int ldp;            // partial row stride (>= max_iter + 2)
   int arn_blocks;     // blocks of the fused Arnoldi step (one per SM, co-resident)
+  int64_t arn_vcap;   // complex elements of a block's staged V slice
   double2* V;         // n x (max_iter + 1), column j at V + j*n
   double2* P;         // 2 x RED_BLOCKS x ldp partials
   double2* h1;        // CGS pass 1 coefficients
