@@ -112,11 +112,24 @@ __device__ bool last_block(int* ticket) {
   return s_last != 0;
 }
 
+// out[c] = sum of the RED_BLOCKS partials P[b, c] (c < ncols): every thread
+// sums a fixed strided subset, then a fixed tree over the block -- all loads
+// in flight at once (a serial sum is one L2 round trip per partial)
 __device__ void reduce_partials(const double2* P, int ldp, int ncols, double2* out) {
-  for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+  __shared__ double2 red[RED_THREADS / 32];
+  for (int c = 0; c < ncols; ++c) {
     double2 s = make_double2(0.0, 0.0);
-    for (int b = 0; b < RED_BLOCKS; ++b) s = cadd(s, ld_cg(P + (int64_t)b * ldp + i));
-    st_cg(out + i, s);
+    for (int b = threadIdx.x; b < RED_BLOCKS; b += RED_THREADS)
+      s = cadd(s, ld_cg(P + (int64_t)b * ldp + c));
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int w = 0; w < RED_THREADS / 32; ++w) t = cadd(t, red[w]);
+      st_cg(out + c, t);
+    }
+    __syncthreads();
   }
 }
 
@@ -379,83 +392,6 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
 
 // ---- kernels -----------------------------------------------------------------
 
-__global__ void __launch_bounds__(RED_THREADS) k_h1(GmresDev g) {
-  if (stopped(g.st)) return;
-  const int j = g.st->iterations;
-  const double2* w = g.V + (int64_t)(j + 1) * g.n;
-  int64_t lo, hi;
-  block_range(g.n, lo, hi);
-  int bad = 0;
-  for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
-    const double2 v = ld_cg(w + e);
-    bad |= !(isfinite(v.x) && isfinite(v.y));
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(g.nonfinite, 1);
-  dots_pass(g.V, g.n, j + 1, w, lo, hi, g.P + (int64_t)blockIdx.x * g.ldp);
-  if (last_block(g.ticket + 0)) {
-    reduce_partials(g.P, g.ldp, j + 1, g.h1);
-    if (threadIdx.x == 0) g.ticket[0] = 0;
-  }
-}
-
-__global__ void __launch_bounds__(RED_THREADS) k_h2(GmresDev g) {
-  if (stopped(g.st)) return;
-  const int j = g.st->iterations;
-  extern __shared__ double2 hs[];
-  const int nc = j + 1;
-  for (int i = threadIdx.x; i < nc; i += RED_THREADS) hs[i] = ld_cg(g.h1 + i);
-  __syncthreads();
-  double2* w = g.V + (int64_t)(j + 1) * g.n;
-  int64_t lo, hi;
-  block_range(g.n, lo, hi);
-  update_pass(g.V, g.n, nc, hs, w, lo, hi);
-  dots_pass(g.V, g.n, nc, w, lo, hi, g.P + (int64_t)blockIdx.x * g.ldp);
-  if (last_block(g.ticket + 1)) {
-    reduce_partials(g.P, g.ldp, nc, g.h2);
-    if (threadIdx.x == 0) g.ticket[1] = 0;
-  }
-}
-
-__global__ void __launch_bounds__(RED_THREADS)
-k_norm_givens(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle cond) {
-  if (stopped(g.st)) return;
-  const int j = g.st->iterations;
-  extern __shared__ double2 hs[];
-  const int nc = j + 1;
-  for (int i = threadIdx.x; i < nc; i += RED_THREADS) hs[i] = ld_cg(g.h2 + i);
-  __syncthreads();
-  double2* w = g.V + (int64_t)(j + 1) * g.n;
-  int64_t lo, hi;
-  block_range(g.n, lo, hi);
-  update_pass(g.V, g.n, nc, hs, w, lo, hi);
-  norm_pass(w, lo, hi, g.P + (int64_t)blockIdx.x * g.ldp);
-  if (last_block(g.ticket + 2)) {
-    reduce_partials(g.P, g.ldp, 1, g.hn2);
-    __syncthreads();
-    __threadfence_block();
-    if (threadIdx.x == 0) {
-      g.ticket[2] = 0;
-      givens_update(g, j, rel_tol, max_iter);
-      if (cond) cudaGraphSetConditional(cond, g.st->stop ? 0u : 1u);
-    }
-  }
-}
-
-// v_{j+1} = w / ||w||; skipped once the solve stopped (column k is unused)
-__global__ void k_normalize(GmresDev g) {
-  const DevStatus* st = g.st;
-  if (stopped(st)) return;
-  const double s = st->inv_hn;
-  double2* w = g.V + (int64_t)st->iterations * g.n;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    double2 v = ld_cg(w + e);
-    v.x *= s;
-    v.y *= s;
-    st_cg(w + e, v);
-  }
-}
-
 __global__ void __launch_bounds__(RED_THREADS)
 k_begin_norm(GmresDev g, cudaGraphConditionalHandle cond) {
   int64_t lo, hi;
@@ -501,18 +437,31 @@ __global__ void k_begin_scale(GmresDev g) {
   }
 }
 
-// R y = g[0:k] (upper triangular k x k, k = iterations); a zero pivot gives y_i = 0
-__global__ void k_backsolve(GmresDev g) {
+// R y = g[0:k] (upper triangular k x k, k = iterations); a zero pivot gives
+// y_i = 0.  One block: R and g in shared memory, column-oriented substitution
+// (y_i, then every g_t, t < i, updated in parallel): k barrier steps instead
+// of k^2 dependent global loads.
+__global__ void __launch_bounds__(RED_THREADS) k_backsolve(GmresDev g) {
+  extern __shared__ double2 rs[];  // k x k (column-major) + g
   const int k = g.st->iterations;
   const int ldr = g.max_iter + 1;
+  double2* gs = rs + (int64_t)k * k;
+  for (int i = threadIdx.x; i < k * k; i += blockDim.x)
+    rs[i] = g.R[(int64_t)(i / k) * ldr + (i % k)];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) gs[i] = g.g[i];
+  __syncthreads();
   for (int i = k - 1; i >= 0; --i) {
-    double2 acc = g.g[i];
-    for (int l = i + 1; l < k; ++l) acc = csub(acc, cmul(g.R[(int64_t)l * ldr + i], g.y[l]));
-    const double2 d = g.R[(int64_t)i * ldr + i];
-    const double dd = cabs2(d);
-    g.y[i] = dd == 0.0 ? make_double2(0.0, 0.0)
-                       : make_double2((acc.x * d.x + acc.y * d.y) / dd,
-                                      (acc.y * d.x - acc.x * d.y) / dd);
+    const double2 d = rs[(int64_t)i * k + i];
+    const double dd = d.x * d.x + d.y * d.y;
+    const double2 acc = gs[i];
+    const double2 yi = dd == 0.0 ? make_double2(0.0, 0.0)
+                                 : make_double2((acc.x * d.x + acc.y * d.y) / dd,
+                                                (acc.y * d.x - acc.x * d.y) / dd);
+    __syncthreads();  // every thread has read gs[i]
+    if (threadIdx.x == 0) g.y[i] = yi;
+    for (int t = threadIdx.x; t < i; t += blockDim.x)
+      gs[t] = csub(gs[t], cmul(rs[(int64_t)i * k + t], yi));
+    __syncthreads();
   }
 }
 
@@ -551,15 +500,11 @@ k_resid(GmresDev g, const double2* b, const double2* ax) {
   }
   block_sum_chunk(acc, red, g.P + (int64_t)blockIdx.x * g.ldp, 2);
   if (last_block(g.ticket + 0)) {
+    reduce_partials(g.P, g.ldp, 2, g.hn2);
     if (threadIdx.x == 0) {
       g.ticket[0] = 0;
-      double a = 0.0, c = 0.0;
-      for (int i = 0; i < RED_BLOCKS; ++i) {
-        a += ld_cg(g.P + (int64_t)i * g.ldp).x;
-        c += ld_cg(g.P + (int64_t)i * g.ldp + 1).x;
-      }
-      g.st->true_num2 = a;
-      g.st->b_norm2 = c;
+      g.st->true_num2 = ld_cg(g.hn2).x;
+      g.st->b_norm2 = ld_cg(g.hn2 + 1).x;
     }
   }
 }
@@ -624,6 +569,16 @@ cudaError_t gm_arnoldi_setup(GmresDev& g, int device) {
                              (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
   }
+  {  // back substitution: R (k x k, k <= max_iter) and g in shared memory
+    static std::atomic<int> bs_max{0};
+    const int need = (int)((size_t)g.max_iter * (g.max_iter + 1) * sizeof(double2));
+    int cur = bs_max.load();
+    while (need > cur && !bs_max.compare_exchange_weak(cur, need)) {
+    }
+    e = cudaFuncSetAttribute(k_backsolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             cur > need ? cur : need);
+    if (e != cudaSuccess) return e;
+  }
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi, ARN_THREADS, smem);
   if (e != cudaSuccess) return e;
@@ -639,7 +594,7 @@ void gm_begin(const GmresDev& g, cudaGraphConditionalHandle cond, cudaStream_t s
 
 void gm_finish(const GmresDev& g, double2* x, cudaStream_t s) {
   count_launch();
-  k_backsolve<<<1, 1, 0, s>>>(g);
+  k_backsolve<<<1, RED_THREADS, (size_t)g.max_iter * (g.max_iter + 1) * sizeof(double2), s>>>(g);
   count_launch();
   k_combine<<<grid_for(g.n), 256, (size_t)(g.max_iter + 1) * sizeof(double2), s>>>(g, x);
 }
