@@ -33,6 +33,10 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "online solve ms & trace-apply HBM GB/s (fraction of peak), n=800², L=16"
+# FP64 tensor-core peak of one B200 measured with tools/dmma_bench.cu
+# (profiles/r01_fp64_dmma_vs_dfma.txt; mma.sync m8n8k4/m16n8k16 .f64)
+FP64_TENSOR_TFLOPS = 36.9
+FP64_PEAK_SRC = "measured (tools/dmma_bench.cu, profiles/r01_fp64_dmma_vs_dfma.txt)"
 FALLBACK_HBM = 6650.0
 L2_BYTES = 126 * 2**20
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -263,9 +267,17 @@ def run_ours(args):
     x = torch.empty_like(b)
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=f"cuda:{local}")
     stream = torch.cuda.current_stream()
+    # multi-source dense workloads (c5) run the sources in lockstep batches on
+    # the batched executor (pt_gmres_batch); single sources the fused path
+    batched = (len(mine) > 1 and meta.get("kernel_format") == "dense"
+               and not os.environ.get("PT_BATCH_SEQ"))
+    B_dev = torch.stack(rhs_dev) if batched else None
 
     def step():
         rep = None
+        if batched:
+            _, reps = op.gmres_batch(B_dev, rel_tol=tol, max_iter=max_iter, n_it=n_it)
+            return reps[0]
         for bs in rhs_dev:
             _, rep = op.gmres(bs, rel_tol=tol, max_iter=max_iter, n_it=n_it, out=x)
         return rep
@@ -322,7 +334,13 @@ def run_ours(args):
     x_host = torch.empty_like(b_host[0]).pin_memory()
     e2e_ms = []
 
+    B_host = torch.stack(b_host).pin_memory() if batched else None
+    X_host = torch.empty_like(B_host).pin_memory() if batched else None
+
     def step_host():
+        if batched:
+            op.gmres_batch_host(B_host, X_host, rel_tol=tol, max_iter=max_iter, n_it=n_it)
+            return
         for bh in b_host:
             op.gmres_host(bh, x_host, rel_tol=tol, max_iter=max_iter, n_it=n_it)
 
@@ -359,6 +377,16 @@ def run_ours(args):
         return
     peak, peak_src = peaks()
     achieved = exec_bytes / (exec_ms * 1e-3) / 1e9 if exec_ms > 0 else None
+    roof_unit, bound = "GB/s", "hbm"
+    if batched:
+        # FP64-tensor-bound: 8 flop per kernel element per source;
+        # peak = the mma.sync .f64 rate measured on this GPU (no FP64 entry in
+        # MEASURED_PEAKS.json)
+        per_batch = min(len(mine), 64)
+        flops = exec_bytes / 16 * 8 * per_batch
+        achieved = flops / (exec_ms * 1e-3) / 1e12 if exec_ms > 0 else None
+        peak, peak_src = FP64_TENSOR_TFLOPS, FP64_PEAK_SRC
+        roof_unit, bound = "TFLOP/s", "tensor"
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
@@ -374,12 +402,16 @@ def run_ours(args):
         "config": workload_config(name, meta, {"iterations": k,
                                                "reference_iterations": (meta["solves"][0]["iterations"]
                                                                         if meta.get("solves") else None),
-                                               "trace_rel_err_vs_reference": trace_err}),
+                                               "trace_rel_err_vs_reference": trace_err,
+                                               "sources": len(mine),
+                                               "batched": ("lockstep batches of 64 (pt_gmres_batch)"
+                                                           if batched else None)}),
         "impl": "ours",
         "roofline": {
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "bound": bound, "achieved": achieved, "peak": peak, "unit": roof_unit,
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": "pt_exec_kernel (operator applies: fused A->M iteration program)",
+            "kernel": ("pt_bexec_kernel (batched A->M iteration program, DMMA)" if batched else
+                       "pt_exec_kernel (operator applies: fused A->M iteration program)"),
             "algorithmic_bytes_per_launch": exec_bytes / max(exec_n, 1),
             "launch_ms_avg": exec_ms / max(exec_n, 1), "launches": exec_n,
             "peak_source": peak_src,
@@ -395,7 +427,8 @@ def run_ours(args):
                   "upload_s": upload_s, "offline_host_s": meta.get("offline_seconds")},
         "e2e": {"value": e2e_total / (args.steps * solves_per_step), "unit": "ms",
                 "h2d_bytes_per_step": N * 16 * len(mine), "d2h_bytes_per_step": N * 16 * len(mine),
-                "api": "pt_gmres_host (C ABI, pinned host b/x)"},
+                "api": ("pt_gmres_batch_host" if batched else "pt_gmres_host")
+                       + " (C ABI, pinned host b/x)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

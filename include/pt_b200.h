@@ -141,11 +141,30 @@ int pt_gmres_host(pt_handle *h, const double *b_host, double *x_host,
                   pt_stream stream);
 
 /* Batched independent solves of nrhs right-hand sides stored column after
- * column (b[s*N ...]); reports[s] per RHS.  Operator applies become
- * multi-RHS contractions (no reference API; cli.py:380-409 loops). */
+ * column (b[s*N ...]); reports[s] per RHS (the per-source loop of
+ * cli.py:380-409, one gmres_solve per source, solver.py:231-295).  Dense
+ * operators run up to 64 sources in lockstep: each kernel row is read once
+ * per iteration for all of them and every block term is a multi-RHS
+ * contraction on the FP64 tensor cores; each source keeps its own status,
+ * flags and iteration count.  PLR operators solve the sources one by one.
+ * Returns PT_ENONFINITE (after filling every report) if any source met
+ * non-finite values. */
 int pt_gmres_batch(pt_handle *h, const double *b, double *x, int32_t nrhs,
                    const pt_gmres_config *cfg, pt_report *reports,
                    pt_stream stream);
+/* Same with HOST b/x (copies inside). */
+int pt_gmres_batch_host(pt_handle *h, const double *b_host, double *x_host,
+                        int32_t nrhs, const pt_gmres_config *cfg,
+                        pt_report *reports, pt_stream stream);
+
+/* Multi-RHS applies on nrhs column-major device vectors (dense operators):
+ * Y[:, s] = pol @ X[:, s] (trace_system.py:219-226) and
+ * Z[:, s] = preconditioner_apply(R[:, s]) (solver.py:223-228) -- the
+ * operators of pt_gmres_batch. */
+int pt_apply_A_batch(pt_handle *h, const double *x, double *y, int32_t nrhs,
+                     pt_stream stream);
+int pt_apply_M_batch(pt_handle *h, const double *r, double *z, int32_t nrhs,
+                     int32_t n_it, pt_stream stream);
 
 /* ---- generic GMRES workspace (callable operators) ------------------------
  * The reference's gmres_solve takes arbitrary callables apply_A/apply_Minv.

@@ -62,6 +62,10 @@ _SIGS = {
     "pt_gmres_host": (C.c_int, [_VP, _VP, _VP, C.POINTER(GmresConfigC), C.POINTER(Report), _VP]),
     "pt_gmres_batch": (C.c_int, [_VP, _VP, _VP, C.c_int32, C.POINTER(GmresConfigC),
                                  C.POINTER(Report), _VP]),
+    "pt_gmres_batch_host": (C.c_int, [_VP, _VP, _VP, C.c_int32, C.POINTER(GmresConfigC),
+                                      C.POINTER(Report), _VP]),
+    "pt_apply_A_batch": (C.c_int, [_VP, _VP, _VP, C.c_int32, _VP]),
+    "pt_apply_M_batch": (C.c_int, [_VP, _VP, _VP, C.c_int32, C.c_int32, _VP]),
     "pt_gmres_ws_create": (C.c_int, [C.c_int64, C.c_int32, C.c_int, C.POINTER(_VP)]),
     "pt_gmres_ws_destroy": (C.c_int, [_VP]),
     "pt_gmres_ws_basis": (_VP, [_VP, C.c_int32]),

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "pt_b200.h"
+#include "pt_batch.cuh"
 #include "pt_device.cuh"
 #include "pt_gmres.cuh"
 #include "pt_plan.h"
@@ -161,6 +162,64 @@ struct pt_handle {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     graphs.clear();
   }
+  // multi-RHS path (pt_batch.cu): dense operators, BW sources per batch
+  struct Batch {
+    std::map<std::string, std::unique_ptr<DevProgram>> progs;
+    PlanParams pp;
+    int grid = 0;  // persistent CTAs of the batched executor
+    double2* slot[N_SLOTS] = {nullptr};
+    int64_t slot_cap[N_SLOTS] = {0};
+    int* ctr = nullptr;
+    int ctr_cap = 0;
+    BGmresDev g{};
+    int g_iter = 0;  // max_iter the GMRES arrays are sized for
+    double2* b = nullptr;     // batched rhs / solution / scratch (N x BW)
+    double2* x = nullptr;
+    double2* tmp = nullptr;
+    double2* cols = nullptr;  // column-major staging of the *_host calls
+    DevStatus* st_host = nullptr;  // pinned: BW statuses + the control words
+    double* hist_host = nullptr;   // pinned: BW x max_iter
+    int* ctl_host = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    struct Graph {
+      int n_it = 0, max_iter = 0, nrhs = 0;
+      double tol = 0.0;
+      int64_t k_pro = 0, k_body = 0, k_epi = 0;
+      cudaGraphExec_t exec = nullptr;
+    };
+    std::vector<Graph> graphs;
+    void drop_graphs() {
+      for (auto& gr : graphs) cudaGraphExecDestroy(gr.exec);
+      graphs.clear();
+    }
+    void free_gmres() {
+      for (void* p : {(void*)g.V, (void*)g.P, (void*)g.h1, (void*)g.h2, (void*)g.R, (void*)g.g,
+                      (void*)g.cs, (void*)g.sn, (void*)g.hist, (void*)g.y, (void*)g.inv,
+                      (void*)g.st, (void*)g.ctl})
+        cudaFree(p);
+      g = BGmresDev{};
+      cudaFreeHost(st_host);
+      cudaFreeHost(hist_host);
+      cudaFreeHost(ctl_host);
+      st_host = nullptr;
+      hist_host = nullptr;
+      ctl_host = nullptr;
+      g_iter = 0;
+    }
+    ~Batch() {
+      drop_graphs();
+      free_gmres();
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+      progs.clear();
+      for (int s = 0; s < N_SLOTS; ++s) cudaFree(slot[s]);
+      cudaFree(ctr);
+      cudaFree(b);
+      cudaFree(x);
+      cudaFree(tmp);
+      cudaFree(cols);
+    }
+  } batch;
   // per-task timeline of one traced launch (pt_trace_program)
   unsigned long long* trace_buf = nullptr;
   // per-launch instrumentation of the executor
@@ -1119,6 +1178,374 @@ bool use_graph(const pt_handle* h) {
   return !h->timing && !(e && e[0] == '0');
 }
 
+// ---- multi-RHS (batched) path ------------------------------------------------
+// Dense operators only: the batched executor streams dense kernel rows (a
+// PLR operator keeps the per-source solves, see pt_gmres_batch).
+
+int batch_init(pt_handle* h) {
+  auto& B = h->batch;
+  if (B.grid > 0) return 0;
+  CK(bexec_setup());
+  CK(bg_setup(1));
+  B.grid = bexec_grid(h->device);
+  if (B.grid <= 0) return fail(PT_ECUDA, "batched executor does not fit on an SM");
+  B.pp = h->pp;
+  B.pp.ctas = B.grid;
+  B.pp.dense_rows_per_task = BT_ROWS;
+  B.pp.row_chunk = BT_ROWS;  // every task its own producer group: finest dependencies
+  B.pp.half_elems = (int64_t)BT_ROWS * h->op.m;
+  // list-scheduling model: a task's cost is its kernel bytes at the
+  // FP64-bound rate of one CTA (BW/2 flop per kernel byte)
+  B.pp.task_us = 1.0;
+  B.pp.cta_gbs = 2.5;
+  if (const char* e = std::getenv("PT_BATCH_CTA_GBS")) B.pp.cta_gbs = std::atof(e);
+  if (const char* e = std::getenv("PT_BATCH_BOOST")) B.pp.chain_boost_us = std::atof(e);
+  const size_t bytes = (size_t)h->N() * BW * sizeof(double2);
+  CK(cudaMalloc(&B.b, bytes));
+  CK(cudaMalloc(&B.x, bytes));
+  CK(cudaMalloc(&B.tmp, bytes));
+  CK(cudaMalloc(&B.cols, bytes));
+  CK(cudaMemset(B.b, 0, bytes));
+  CK(cudaMemset(B.x, 0, bytes));
+  for (auto& e : B.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return 0;
+}
+
+int ensure_bslot(pt_handle* h, int s, int64_t elems) {
+  auto& B = h->batch;
+  if (elems <= B.slot_cap[s]) return 0;
+  CK(cudaDeviceSynchronize());
+  B.drop_graphs();
+  cudaFree(B.slot[s]);
+  CK(cudaMalloc(&B.slot[s], (size_t)elems * BW * sizeof(double2)));
+  CK(cudaMemset(B.slot[s], 0, (size_t)elems * BW * sizeof(double2)));
+  B.slot_cap[s] = elems;
+  return 0;
+}
+
+int get_bprogram(pt_handle* h, const std::string& kind, int n_it, DevProgram** out) {
+  auto& B = h->batch;
+  int rc;
+  if ((rc = batch_init(h))) return rc;
+  const std::string key = kind + std::to_string(n_it);
+  auto it = B.progs.find(key);
+  if (it != B.progs.end()) {
+    *out = it->second.get();
+    return 0;
+  }
+  std::unique_ptr<DevProgram> p(new DevProgram());
+  if (kind == "A")
+    p->host = build_apply_A(h->op, B.pp);
+  else if (kind == "M")
+    p->host = build_apply_M(h->op, n_it, B.pp);
+  else
+    p->host = build_A_then_M(h->op, n_it, B.pp);
+  if (!p->host.overflow.empty()) return fail(PT_EINVAL, p->host.overflow);
+  for (const DevTask& t : p->host.tasks)
+    if (t.type != TASK_Y_DENSE || t.nterm > BT_TERMS || t.neye > BT_EYES || t.r1 - t.r0 > BT_ROWS)
+      return fail(PT_EINVAL, "a task exceeds what the batched executor stages");
+  if ((rc = upload(&p->tasks, p->host.tasks))) return rc;
+  if ((rc = upload(&p->terms, p->host.terms))) return rc;
+  if ((rc = upload(&p->eyes, p->host.eyes))) return rc;
+  if ((rc = upload(&p->waits, p->host.waits))) return rc;
+  for (int s : {SLOT_Y, SLOT_U1, SLOT_U2, SLOT_PRE})
+    if ((rc = ensure_bslot(h, s, p->host.slot_elems[s]))) return rc;
+  if (p->host.n_counters + 1 > B.ctr_cap) {
+    CK(cudaDeviceSynchronize());
+    B.drop_graphs();
+    cudaFree(B.ctr);
+    B.ctr_cap = p->host.n_counters + 1;
+    CK(cudaMalloc(&B.ctr, B.ctr_cap * sizeof(int)));
+  }
+  *out = p.get();
+  B.progs[key] = std::move(p);
+  return 0;
+}
+
+int run_bprogram(pt_handle* h, DevProgram* p, const double2* in, double2* out, cudaStream_t s,
+                 const int* stop = nullptr, const int* iter = nullptr, double2* vbase = nullptr,
+                 int64_t vstride = 0) {
+  auto& B = h->batch;
+  if (p->host.tasks.empty()) return 0;
+  BExecArgs a{};
+  a.tasks = p->tasks;
+  a.terms = p->terms;
+  a.eyes = p->eyes;
+  a.waits = p->waits;
+  a.ctr = B.ctr;
+  a.head = B.ctr + p->host.n_counters;
+  for (int i = 0; i < N_SLOTS; ++i) a.slot[i] = B.slot[i];
+  a.slot[SLOT_IN] = const_cast<double2*>(in);
+  a.slot[SLOT_OUT] = out;
+  a.dense = h->dense;
+  a.n_tasks = (int)p->host.tasks.size();
+  a.m = (int)h->op.m;
+  a.stop = stop;
+  a.iter = iter;
+  a.vbase = vbase;
+  a.vstride = vstride;
+  CK(cudaMemsetAsync(B.ctr, 0, (p->host.n_counters + 1) * sizeof(int), s));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing) {
+    for (cudaEvent_t* e : {&e0, &e1}) {
+      if (h->ev_free.empty()) {
+        CK(cudaEventCreate(e));
+      } else {
+        *e = h->ev_free.back();
+        h->ev_free.pop_back();
+      }
+    }
+    CK(cudaEventRecord(e0, s));
+  }
+  CK(bexec_launch(a, B.grid, s));
+  if (h->timing) {
+    CK(cudaEventRecord(e1, s));
+    h->ev_used.emplace_back(e0, e1);
+    h->timed_launches += 1;
+    h->timed_bytes += p->host.algo_bytes;
+  }
+  return 0;
+}
+
+int ensure_bgws(pt_handle* h, int max_iter) {
+  auto& B = h->batch;
+  if (B.g_iter >= max_iter) return 0;
+  CK(cudaDeviceSynchronize());
+  B.drop_graphs();
+  B.free_gmres();
+  BGmresDev& g = B.g;
+  const int64_t N = h->N();
+  const size_t ldr = (size_t)max_iter + 1;
+  g.n = N;
+  g.max_iter = max_iter;
+  CK(cudaMalloc(&g.V, ldr * N * BW * sizeof(double2)));
+  CK(cudaMalloc(&g.P, (size_t)BRED_BLOCKS * ldr * BW * sizeof(double2)));
+  CK(cudaMalloc(&g.h1, ldr * BW * sizeof(double2)));
+  CK(cudaMalloc(&g.h2, ldr * BW * sizeof(double2)));
+  CK(cudaMalloc(&g.R, (size_t)BW * ldr * max_iter * sizeof(double2)));
+  CK(cudaMalloc(&g.g, (size_t)BW * ldr * sizeof(double2)));
+  CK(cudaMalloc(&g.cs, (size_t)BW * max_iter * sizeof(double)));
+  CK(cudaMalloc(&g.sn, (size_t)BW * max_iter * sizeof(double2)));
+  CK(cudaMalloc(&g.hist, (size_t)BW * max_iter * sizeof(double)));
+  CK(cudaMalloc(&g.y, (size_t)BW * max_iter * sizeof(double2)));
+  CK(cudaMalloc(&g.inv, BW * sizeof(double)));
+  CK(cudaMalloc(&g.st, BW * sizeof(DevStatus)));
+  CK(cudaMalloc(&g.ctl, 4 * sizeof(int)));
+  CK(cudaMemset(g.V, 0, ldr * N * BW * sizeof(double2)));
+  CK(cudaMemset(g.st, 0, BW * sizeof(DevStatus)));
+  CK(cudaMemset(g.ctl, 0, 4 * sizeof(int)));
+  CK(cudaMallocHost(&B.st_host, BW * sizeof(DevStatus)));
+  CK(cudaMallocHost(&B.hist_host, (size_t)BW * max_iter * sizeof(double)));
+  CK(cudaMallocHost(&B.ctl_host, 2 * 4 * sizeof(int)));
+  CK(bg_setup(max_iter));
+  B.g_iter = max_iter;
+  return 0;
+}
+
+// One batch of up to BW sources, already packed into B.b; solution in B.x,
+// statuses and histories in the pinned host arrays.  Whole solve as one CUDA
+// graph (conditional WHILE over the lockstep iterations) unless per-launch
+// timing is on; then a host loop one step ahead of its stop check.
+int bgmres_run(pt_handle* h, const pt_gmres_config* cfg, int nrhs, cudaStream_t s) {
+  auto& B = h->batch;
+  int rc;
+  DevProgram *pM, *pAM, *pA;
+  if ((rc = get_bprogram(h, "M", cfg->n_it, &pM))) return rc;
+  if ((rc = get_bprogram(h, "AM", cfg->n_it, &pAM))) return rc;
+  if ((rc = get_bprogram(h, "A", 0, &pA))) return rc;
+  if ((rc = ensure_bgws(h, cfg->max_iter))) return rc;
+  BGmresDev g = B.g;
+  g.max_iter = B.g_iter;
+  g.nrhs = nrhs;
+  const int64_t N = h->N();
+  const int64_t vstride = N * BW;
+  auto epilogue = [&](cudaStream_t cs) -> int {
+    bg_finish(g, B.x, cs);
+    int r = run_bprogram(h, pA, B.x, B.tmp, cs);
+    if (r) return r;
+    bg_resid(g, B.b, B.tmp, cs);
+    CK(cudaMemcpyAsync(B.st_host, g.st, BW * sizeof(DevStatus), cudaMemcpyDeviceToHost, cs));
+    CK(cudaMemcpyAsync(B.hist_host, g.hist, (size_t)BW * g.max_iter * sizeof(double),
+                       cudaMemcpyDeviceToHost, cs));
+    return 0;
+  };
+  if (!use_graph(h)) {
+    if ((rc = run_bprogram(h, pM, B.b, g.V, s))) return rc;
+    bg_begin(g, 0, s);
+    int enq = 0, nb = 0, waited = 0;
+    auto enqueue = [&]() -> int {
+      for (int i = 0; i < 2 && enq < cfg->max_iter; ++i, ++enq) {
+        int r = run_bprogram(h, pAM, nullptr, nullptr, s, g.ctl + 1, g.ctl, g.V, vstride);
+        if (r) return r;
+        bg_step(g, cfg->rel_tol, cfg->max_iter, 0, s);
+      }
+      CK(cudaMemcpyAsync(B.ctl_host + 4 * (nb % 2), g.ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(B.ev[nb % 2], s));
+      ++nb;
+      return 0;
+    };
+    if ((rc = enqueue())) return rc;
+    for (;;) {
+      if (enq < cfg->max_iter && (rc = enqueue())) return rc;
+      CK(cudaEventSynchronize(B.ev[waited % 2]));
+      const int stop = B.ctl_host[4 * (waited % 2) + 1];
+      ++waited;
+      if (stop) break;
+      if (waited == nb && enq >= cfg->max_iter) break;
+    }
+    if ((rc = epilogue(s))) return rc;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return 0;
+  }
+  pt_handle::Batch::Graph* gr = nullptr;
+  for (auto& x : B.graphs)
+    if (x.n_it == cfg->n_it && x.max_iter == cfg->max_iter && x.tol == cfg->rel_tol && x.nrhs == nrhs)
+      gr = &x;
+  if (!gr) {
+    if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t cs = h->cap_stream;
+    cudaGraph_t graph = nullptr, tmp = nullptr;
+    CK(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    const int64_t c0 = g_launches.load();
+    CK(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    rc = run_bprogram(h, pM, B.b, g.V, cs);
+    if (!rc) bg_begin(g, cond, cs);
+    cudaStreamCaptureStatus cst;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaError_t ce = cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps);
+    std::vector<cudaGraphNode_t> tail(deps, deps + ndeps);
+    CK(cudaStreamEndCapture(cs, &tmp));
+    if (rc) return rc;
+    CK(ce);
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop;
+    CK(cudaGraphAddNode(&loop, graph, tail.data(), tail.size(), &cp));
+    const int64_t c1 = g_launches.load();
+    CK(cudaStreamBeginCaptureToGraph(cs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    rc = run_bprogram(h, pAM, nullptr, nullptr, cs, g.ctl + 1, g.ctl, g.V, vstride);
+    if (!rc) bg_step(g, cfg->rel_tol, cfg->max_iter, cond, cs);
+    CK(cudaStreamEndCapture(cs, &tmp));
+    if (rc) return rc;
+    const int64_t c2 = g_launches.load();
+    CK(cudaStreamBeginCaptureToGraph(cs, graph, &loop, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+    rc = epilogue(cs);
+    CK(cudaStreamEndCapture(cs, &tmp));
+    if (rc) return rc;
+    pt_handle::Batch::Graph ng;
+    CK(cudaGraphInstantiate(&ng.exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    const int64_t c3 = g_launches.load();
+    ng.k_pro = c1 - c0;
+    ng.k_body = c2 - c1;
+    ng.k_epi = c3 - c2;
+    g_launches.fetch_sub(c3 - c0);
+    ng.n_it = cfg->n_it;
+    ng.max_iter = cfg->max_iter;
+    ng.tol = cfg->rel_tol;
+    ng.nrhs = nrhs;
+    B.graphs.push_back(ng);
+    gr = &B.graphs.back();
+  }
+  CK(cudaGraphLaunch(gr->exec, s));
+  CK(cudaStreamSynchronize(s));
+  int iters = 0;
+  for (int k = 0; k < BW; ++k) iters = std::max(iters, B.st_host[k].iterations);
+  g_launches.fetch_add(gr->k_pro + (int64_t)iters * gr->k_body + gr->k_epi);
+  return 0;
+}
+
+// per-source reports of the last batch (sources [0, nrhs)); PT_ENONFINITE if
+// any source met non-finite values
+int bgmres_reports(pt_handle* h, int nrhs, int max_iter, int first, pt_report* reports) {
+  auto& B = h->batch;
+  int bad = -1;
+  for (int k = 0; k < nrhs; ++k) {
+    const DevStatus& st = B.st_host[k];
+    if (st.nonfinite && bad < 0) bad = k;
+    if (!reports) continue;
+    pt_report* rep = reports + first + k;
+    double* hist = rep->residual_history;
+    *rep = pt_report{};
+    rep->residual_history = hist;
+    fill_report(st, rep);
+    if (hist && st.iterations > 0)
+      std::memcpy(hist, B.hist_host + (size_t)k * B.g_iter, (size_t)st.iterations * sizeof(double));
+    if (st.beta == 0.0) {
+      rep->converged = 1;
+      rep->flag = PT_FLAG_CONVERGED;
+      rep->true_residual = 0.0;
+    } else {
+      const double tr = std::sqrt(st.true_num2), sc = std::sqrt(st.b_norm2);
+      rep->true_residual = sc > 0.0 ? tr / sc : tr;
+    }
+  }
+  (void)max_iter;
+  if (bad >= 0)
+    return fail(PT_ENONFINITE, "non-finite values in preconditioned matvec at iteration " +
+                                   std::to_string(B.st_host[bad].iterations + 1) + " (source " +
+                                   std::to_string(first + bad) + ")");
+  return 0;
+}
+
+// batched solve of nrhs column-major sources (device or host buffers)
+int gmres_batched(pt_handle* h, const double2* b, double2* x, int nrhs, bool host,
+                  const pt_gmres_config* cfg, pt_report* reports, cudaStream_t s) {
+  int rc;
+  if ((rc = batch_init(h))) return rc;
+  auto& B = h->batch;
+  const int64_t N = h->N();
+  int status = 0;
+  for (int first = 0; first < nrhs; first += BW) {
+    const int nb = std::min(BW, nrhs - first);
+    const double2* src = b + (size_t)first * N;
+    if (host) {
+      CK(cudaMemcpyAsync(B.cols, src, (size_t)nb * N * sizeof(double2), cudaMemcpyHostToDevice, s));
+      src = B.cols;
+    }
+    b_pack(src, N, nb, B.b, s);
+    CK(cudaGetLastError());
+    if ((rc = bgmres_run(h, cfg, nb, s))) return rc;
+    double2* dst = host ? B.cols : x + (size_t)first * N;
+    b_unpack(B.x, N, nb, dst, s);
+    CK(cudaGetLastError());
+    if (host)
+      CK(cudaMemcpyAsync(x + (size_t)first * N, B.cols, (size_t)nb * N * sizeof(double2),
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    rc = bgmres_reports(h, nb, cfg->max_iter, first, reports);
+    if (rc && !status) status = rc;
+  }
+  return status;
+}
+
+// batched apply of kind "A" or "M" to nrhs column-major device vectors
+int apply_batched(pt_handle* h, const std::string& kind, int n_it, const double2* in, double2* out,
+                  int nrhs, cudaStream_t s) {
+  int rc;
+  DevProgram* p;
+  if ((rc = get_bprogram(h, kind, n_it, &p))) return rc;
+  auto& B = h->batch;
+  const int64_t N = h->N();
+  for (int first = 0; first < nrhs; first += BW) {
+    const int nb = std::min(BW, nrhs - first);
+    b_pack(in + (size_t)first * N, N, nb, B.b, s);
+    if ((rc = run_bprogram(h, p, B.b, B.tmp, s))) return rc;
+    b_unpack(B.tmp, N, nb, out + (size_t)first * N, s);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -1172,12 +1599,60 @@ int pt_gmres_batch(pt_handle* h, const double* b, double* x, int32_t nrhs,
                    const pt_gmres_config* cfg, pt_report* reports, pt_stream stream) {
   if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !b || !x || nrhs < 0) return fail(PT_EINVAL, "bad argument");
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
   const int64_t N = h->N();
+  if (h->op.fmt == PT_KERNEL_DENSE && nrhs > 1 && !std::getenv("PT_BATCH_SEQ")) {
+    DeviceGuard guard(h->device);
+    return gmres_batched(h, (const double2*)b, (double2*)x, nrhs, false, cfg, reports,
+                         (cudaStream_t)stream);
+  }
   for (int32_t r = 0; r < nrhs; ++r) {
-    int rc = pt_gmres(h, b + 2 * r * N, x + 2 * r * N, cfg, reports ? reports + r : nullptr, stream);
+    rc = pt_gmres(h, b + 2 * r * N, x + 2 * r * N, cfg, reports ? reports + r : nullptr, stream);
     if (rc) return rc;
   }
   return 0;
+}
+
+int pt_gmres_batch_host(pt_handle* h, const double* b_host, double* x_host, int32_t nrhs,
+                        const pt_gmres_config* cfg, pt_report* reports, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
+  if (!h || !b_host || !x_host || nrhs < 0) return fail(PT_EINVAL, "bad argument");
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  const int64_t N = h->N();
+  if (h->op.fmt == PT_KERNEL_DENSE && nrhs > 1 && !std::getenv("PT_BATCH_SEQ")) {
+    DeviceGuard guard(h->device);
+    return gmres_batched(h, (const double2*)b_host, (double2*)x_host, nrhs, true, cfg, reports,
+                         (cudaStream_t)stream);
+  }
+  for (int32_t r = 0; r < nrhs; ++r) {
+    rc = pt_gmres_host(h, b_host + 2 * r * N, x_host + 2 * r * N, cfg, reports ? reports + r : nullptr,
+                       stream);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int pt_apply_A_batch(pt_handle* h, const double* x, double* y, int32_t nrhs, pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
+  if (!h || !x || !y || nrhs < 0) return fail(PT_EINVAL, "bad argument");
+  if (h->op.fmt != PT_KERNEL_DENSE) return fail(PT_EINVAL, "batched applies need a dense operator");
+  DeviceGuard guard(h->device);
+  return apply_batched(h, "A", 0, (const double2*)x, (double2*)y, nrhs, (cudaStream_t)stream);
+}
+
+int pt_apply_M_batch(pt_handle* h, const double* r, double* z, int32_t nrhs, int32_t n_it,
+                     pt_stream stream) {
+  if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
+  if (!h || !r || !z || nrhs < 0) return fail(PT_EINVAL, "bad argument");
+  if (n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
+  if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  if (h->op.fmt != PT_KERNEL_DENSE) return fail(PT_EINVAL, "batched applies need a dense operator");
+  DeviceGuard guard(h->device);
+  return apply_batched(h, "M", n_it, (const double2*)r, (double2*)z, nrhs, (cudaStream_t)stream);
 }
 
 int pt_gmres_ws_create(int64_t n, int32_t max_iter, int device, pt_gmres_ws** out) {

@@ -246,6 +246,70 @@ class DeviceOperator:
         nat.check(rc, "pt_gmres_host")
         return _report_dict(rep, hist)
 
+    # ---- multi-RHS (one row per source; the reference loops sources,
+    # cli.py:380-409) ------------------------------------------------------
+    def _dev_block(self, X, name="sources"):
+        """(nrhs x N complex128 tensor on the device, was_numpy)."""
+        torch = _torch()
+        if isinstance(X, torch.Tensor):
+            if X.dtype != torch.complex128 or X.device.type != "cuda" or X.device.index != self.device:
+                raise ValueError(f"{name} must be a complex128 tensor on cuda:{self.device}")
+            if X.ndim != 2 or X.shape[1] != self.N:
+                raise ValueError(f"{name} must have shape (nrhs, {self.N}), got {tuple(X.shape)}")
+            return X.contiguous(), False
+        a = np.asarray(X, dtype=np.complex128)
+        if a.ndim != 2 or a.shape[1] != self.N:
+            raise ValueError(f"{name} must have shape (nrhs, {self.N}), got {a.shape}")
+        return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}"), True
+
+    def apply_A_batch(self, X):
+        """Y[s] = pol @ X[s] for every source row s (dense operators)."""
+        Xd, host = self._dev_block(X)
+        Y = _torch().empty_like(Xd)
+        nat.check(nat.lib().pt_apply_A_batch(self._h, Xd.data_ptr(), Y.data_ptr(), int(Xd.shape[0]),
+                                             self.stream()), "pt_apply_A_batch")
+        return self._ret(Y, host)
+
+    def apply_M_batch(self, R, n_it=2):
+        """Z[s] = preconditioner_apply(R[s]) for every source row s (dense operators)."""
+        Rd, host = self._dev_block(R)
+        Z = _torch().empty_like(Rd)
+        nat.check(nat.lib().pt_apply_M_batch(self._h, Rd.data_ptr(), Z.data_ptr(), int(Rd.shape[0]),
+                                             int(n_it), self.stream()), "pt_apply_M_batch")
+        return self._ret(Z, host)
+
+    @staticmethod
+    def _reports(nrhs, max_iter):
+        hists = [(C.c_double * int(max_iter))() for _ in range(nrhs)]
+        reps = (nat.Report * max(nrhs, 1))()
+        for i in range(nrhs):
+            reps[i].residual_history = C.cast(hists[i], C.POINTER(C.c_double))
+        return reps, hists
+
+    def gmres_batch(self, B, rel_tol=1e-7, max_iter=100, n_it=2):
+        """Independent GMRES solves of every source row of B: (X, [report, ...]).
+        Dense operators run the sources in lockstep batches of 64."""
+        Bd, host = self._dev_block(B, "b")
+        X = _torch().empty_like(Bd)
+        nrhs = int(Bd.shape[0])
+        cfg = nat.GmresConfigC(float(rel_tol), int(max_iter), int(n_it))
+        reps, hists = self._reports(nrhs, max_iter)
+        rc = nat.lib().pt_gmres_batch(self._h, Bd.data_ptr(), X.data_ptr(), nrhs, C.byref(cfg), reps,
+                                      self.stream())
+        nat.check(rc, "pt_gmres_batch")
+        return self._ret(X, host), [_report_dict(reps[i], hists[i]) for i in range(nrhs)]
+
+    def gmres_batch_host(self, B_host, X_host, rel_tol=1e-7, max_iter=100, n_it=2):
+        """Batched GMRES from HOST buffers (nrhs x N, pinned torch or numpy)."""
+        nrhs = int(B_host.shape[0])
+        cfg = nat.GmresConfigC(float(rel_tol), int(max_iter), int(n_it))
+        reps, hists = self._reports(nrhs, max_iter)
+        bp = B_host.data_ptr() if hasattr(B_host, "data_ptr") else B_host.ctypes.data
+        xp = X_host.data_ptr() if hasattr(X_host, "data_ptr") else X_host.ctypes.data
+        rc = nat.lib().pt_gmres_batch_host(self._h, bp, xp, nrhs, C.byref(cfg), reps, self.stream())
+        nat.check(rc, "pt_gmres_batch_host")
+        return [_report_dict(reps[i], hists[i]) for i in range(nrhs)]
+
     def exec_timing(self, enable=True):
         """Bracket every executor launch with CUDA events (resets the stats)."""
         nat.check(nat.lib().pt_exec_timing(self._h, 1 if enable else 0), "pt_exec_timing")
