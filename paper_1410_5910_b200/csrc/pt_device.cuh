@@ -10,7 +10,10 @@ namespace pt {
 // executor CTA (one per SM): 16 consumer warps + 2 producer warps (one per
 // task slot)
 constexpr int EXEC_CONSUMERS = 512;
-constexpr int EXEC_PRODUCERS = 2;
+#ifndef PT_EXEC_PRODUCERS
+#define PT_EXEC_PRODUCERS 3
+#endif
+constexpr int EXEC_PRODUCERS = PT_EXEC_PRODUCERS;  // = task slots
 constexpr int EXEC_THREADS = EXEC_CONSUMERS + 32 * EXEC_PRODUCERS;
 constexpr int EXEC_WARPS = EXEC_CONSUMERS / 32;
 constexpr int EXEC_MAX_STAGES = 8;  // operator piece ring (TMA bulk copies); the

@@ -51,6 +51,14 @@ __shared__ volatile int s_grab_turn;     // slot use whose task may be grabbed n
 // stage's previous occupant to be consumed).
 __shared__ volatile int s_resv_turn;     // slot use that reserves positions next
 __shared__ volatile uint32_t s_next_pos; // first unreserved ring position
+// Ring positions fully consumed (a lower bound: updated by the consumers at
+// the end of every task).  A stage's empty barrier is tested by parity, which
+// only tells apart two consecutive phases; a producer therefore looks at
+// position pos only while pos < s_consumed + 2 * n_stages (then the phase of
+// pos - n_stages is the current or the previous one).  Without the bound a
+// producer several uses ahead (long tasks, or more than two task slots) could
+// read an older phase as complete.
+__shared__ volatile uint32_t s_consumed;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -214,7 +222,9 @@ __device__ __forceinline__ void issue_piece(const ExecArgs& a, const Layout& L, 
 // position pos - n_stages, consumed)?
 __device__ __forceinline__ bool stage_free(const Layout& L, uint32_t pos) {
   const uint32_t ns = (uint32_t)L.n_stages;
-  return pos < ns || bar_test(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
+  if (pos < ns) return true;
+  if (pos >= s_consumed + 2 * ns) return false;  // outside the parity window
+  return bar_test(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
 }
 
 // Term scales, eye coefficients and the vector pointers the staging
@@ -329,7 +339,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
   const Slot sl = L.slot(k);
   int n_staged = 0;  // phases of this slot's staging barrier
   for (int j = 0;; ++j) {
-    const int use = 2 * j + k;
+    const int use = EXEC_TSLOTS * j + k;
     if (j > 0) {  // consumers done with use - 2: publish its outputs
       bar_wait(&s_tempty[k], (j - 1) & 1);
       if (lane == 0) {  // release: the consumers' outputs before the count
@@ -401,7 +411,10 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
       // the rest of the task's pieces, as their stages free up
       for (; issued < t.npiece; ++issued) {
         const uint32_t pos = pos0 + issued;
-        if (pos >= ns) bar_wait(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
+        if (pos >= ns) {
+          while (pos >= s_consumed + 2 * ns) __nanosleep(32);
+          bar_wait(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
+        }
         issue_piece(a, L, sl, q, issued, pos);
       }
     }
@@ -575,6 +588,8 @@ __device__ void consumer(const ExecArgs& a, const Layout& L) {
       run_y_dense(a, t, sl, L, rg, q);
     consumer_sync();
     if (threadIdx.x == 0) {  // the slot's producer warp publishes the outputs
+      s_consumed = s_consumed + (uint32_t)t.npiece;  // every warp released the task's stages
+      __threadfence_block();
       trace_mark(a, q, 2);
       trace_mark(a, q, 3);
       if (a.trace) {
@@ -610,6 +625,7 @@ __global__ void __launch_bounds__(EXEC_THREADS, 1) pt_exec_kernel(ExecArgs a) {
     s_resv_turn = 0;
     s_grab_turn = 0;
     s_next_pos = 0;
+    s_consumed = 0;
     for (int i = 0; i < a.n_stages; ++i) {
       bar_init(&s_full[i], 1);
       bar_init(&s_empty[i], EXEC_CONSUMERS / 32);

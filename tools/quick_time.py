@@ -28,9 +28,11 @@ def timed(fn, reps=10):
 
 
 for name in sys.argv[1:]:
-    path = ROOT / "cases" / f"{name}.ptc"
-    if not path.exists():
+    if name.startswith("fx_"):
         path = ROOT / "tests" / "golden" / f"{name}.ptc"
+    else:
+        from paper_1410_5910_b200.offline.build import ensure_case
+        path = ensure_case(name)
     if not path.exists():
         print(name, "missing")
         continue
