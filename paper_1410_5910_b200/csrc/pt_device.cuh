@@ -112,6 +112,7 @@ struct ExecArgs {
   int64_t slot_bytes;        // bytes of one task slot
   int32_t n_stages;          // ring stages (<= EXEC_MAX_STAGES)
   int32_t poll_ns;           // back-off between dependency polls (0: spin)
+  int32_t poll_stagger;      // cycles between the staggered lanes' first polls (0: off)
   const int* stop;  // GMRES status stop flag: the whole launch is skipped once set
   // iteration-relative basis addressing (GMRES loop inside a graph):
   // if iter != nullptr, SLOT_IN = vbase + (*iter) * vstride, SLOT_OUT = SLOT_IN + vstride

@@ -59,6 +59,8 @@ __shared__ volatile uint32_t s_next_pos; // first unreserved ring position
 // producer several uses ahead (long tasks, or more than two task slots) could
 // read an older phase as complete.
 __shared__ volatile uint32_t s_consumed;
+__shared__ volatile unsigned s_seen[EXEC_TSLOTS];  // counters seen satisfied (staggered polling)
+constexpr int POLL_LANES = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -392,14 +394,41 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     }
     {  // dependencies: the lanes poll the task's counters in parallel
       const DevWait* w = sl.waits();
+      const int nw = t.nwait;
       bool ok = true;
-      do {
-        ok = true;
-        for (int i = lane; i < t.nwait; i += 32)
-          if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
-        ok = __all_sync(0xffffffffu, ok);
-        if (!ok && a.poll_ns > 0) __nanosleep(a.poll_ns);
-      } while (!ok);
+      for (int i = lane; i < nw; i += 32)
+        if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
+      ok = __all_sync(0xffffffffu, ok);
+      if (!ok && a.poll_stagger > 0 && nw * POLL_LANES <= 32) {
+        // few counters: POLL_LANES lanes per counter, their polls staggered
+        // over one L2 round trip, so a counter is sampled every ~RTT/POLL_LANES
+        // instead of once per round trip; the first lane to see it satisfied
+        // (acquire) flags it for the others
+        if (lane == 0) s_seen[k] = 0u;
+        __syncwarp();
+        if (lane < nw * POLL_LANES) {
+          const int c = lane % nw, rank = lane / nw;
+          const long long t0 = clock64();
+          while (clock64() - t0 < (long long)rank * a.poll_stagger) {
+          }
+          for (;;) {
+            if ((s_seen[k] >> c) & 1u) break;
+            if (ld_acquire(a.ctr + w[c].ctr) >= w[c].val) {
+              atomicOr((unsigned*)&s_seen[k], 1u << c);
+              break;
+            }
+          }
+        }
+        __syncwarp();
+      } else {
+        while (!ok) {
+          if (a.poll_ns > 0) __nanosleep(a.poll_ns);
+          ok = true;
+          for (int i = lane; i < nw; i += 32)
+            if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
+          ok = __all_sync(0xffffffffu, ok);
+        }
+      }
     }
     if (lane == 0) trace_mark(a, q, 1);
     __syncwarp();
