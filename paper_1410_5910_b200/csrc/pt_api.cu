@@ -168,6 +168,7 @@ struct pt_handle {
     std::map<std::string, std::unique_ptr<DevProgram>> progs;
     PlanParams pp;
     int grid = 0;  // persistent CTAs of the batched executor
+    int rows = BT_ROWS;  // output rows per task (8 or 16)
     double2* slot[N_SLOTS] = {nullptr};
     int64_t slot_cap[N_SLOTS] = {0};
     int* ctr = nullptr;
@@ -1192,13 +1193,14 @@ int batch_init(pt_handle* h) {
   if (B.grid > 0) return 0;
   CK(bexec_setup());
   CK(bg_setup(1));
-  B.grid = bexec_grid(h->device);
+  if (const char* e = std::getenv("PT_BATCH_ROWS")) B.rows = std::atoi(e) == 16 ? 16 : 8;
+  B.grid = bexec_grid(h->device, B.rows);
   if (B.grid <= 0) return fail(PT_ECUDA, "batched executor does not fit on an SM");
   B.pp = h->pp;
   B.pp.ctas = B.grid;
-  B.pp.dense_rows_per_task = BT_ROWS;
-  B.pp.row_chunk = BT_ROWS;  // every task its own producer group: finest dependencies
-  B.pp.half_elems = (int64_t)BT_ROWS * h->op.m;
+  B.pp.dense_rows_per_task = B.rows;
+  B.pp.row_chunk = B.rows;  // every task its own producer group: finest dependencies
+  B.pp.half_elems = (int64_t)B.rows * h->op.m;
   // list-scheduling model: a task's cost is its kernel bytes at the
   // FP64-bound rate of one CTA (BW/2 flop per kernel byte)
   B.pp.task_us = 1.0;
@@ -1247,7 +1249,7 @@ int get_bprogram(pt_handle* h, const std::string& kind, int n_it, DevProgram** o
     p->host = build_A_then_M(h->op, n_it, B.pp);
   if (!p->host.overflow.empty()) return fail(PT_EINVAL, p->host.overflow);
   for (const DevTask& t : p->host.tasks)
-    if (t.type != TASK_Y_DENSE || t.nterm > BT_TERMS || t.neye > BT_EYES || t.r1 - t.r0 > BT_ROWS)
+    if (t.type != TASK_Y_DENSE || t.nterm > BT_TERMS || t.neye > BT_EYES || t.r1 - t.r0 > B.rows)
       return fail(PT_EINVAL, "a task exceeds what the batched executor stages");
   if ((rc = upload(&p->tasks, p->host.tasks))) return rc;
   if ((rc = upload(&p->terms, p->host.terms))) return rc;
@@ -1302,7 +1304,7 @@ int run_bprogram(pt_handle* h, DevProgram* p, const double2* in, double2* out, c
     }
     CK(cudaEventRecord(e0, s));
   }
-  CK(bexec_launch(a, B.grid, s));
+  CK(bexec_launch(a, B.grid, B.rows, s));
   if (h->timing) {
     CK(cudaEventRecord(e1, s));
     h->ev_used.emplace_back(e0, e1);

@@ -30,12 +30,13 @@ namespace {
 
 constexpr int AS_LD = BT_KC + 4;  // A rows 4 apart mod 8 (16-byte units): conflict-free fragments
 constexpr int XS_LD = BW + 2;     // X rows 2 apart mod 8: conflict-free B fragments
-constexpr int AS_ELEMS = BT_ROWS * AS_LD;
 constexpr int XS_ELEMS = BT_KC * XS_LD;
-constexpr size_t BEXEC_SMEM = (size_t)(2 * AS_ELEMS + 2 * XS_ELEMS) * sizeof(double2);
-static_assert(BT_ROWS * BT_KC == BT_THREADS, "one A copy per thread per chunk");
+template <int ROWS>
+constexpr size_t bexec_smem() {
+  return (size_t)(2 * ROWS * AS_LD + 2 * XS_ELEMS) * sizeof(double2);
+}
 static_assert(BT_KC * BW == 4 * BT_THREADS, "four X values per thread per chunk");
-static_assert(BT_ROWS == 16 && BW == 64, "warp tiling: 2 row groups x 4 column groups");
+static_assert(BW == 64 && BT_THREADS == 256, "warp tiling assumes 8 warps over 64 sources");
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -56,10 +57,17 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// ROWS = 16: 8 warps = 2 row groups x 4 column groups of 16 sources (two
+// n-tiles each); ROWS = 8: 1 row group x 8 column groups of 8 sources.
+template <int ROWS>
 __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BExecArgs a) {
+  constexpr int RG = ROWS / 8;           // row groups of 8
+  constexpr int CG = 8 / RG;             // column groups
+  constexpr int NT = BW / CG / 8;        // n-tiles (8 sources) per warp
+  constexpr int AS_ELEMS = ROWS * AS_LD;
   extern __shared__ __align__(16) double2 bsm[];
-  double2* As = bsm;                 // [2][BT_ROWS][AS_LD]  kernel rows of the chunk
-  double2* Xs = bsm + 2 * AS_ELEMS;  // [2][BT_KC][XS_LD]    scaled sources of the chunk
+  double2* As = bsm;                 // [2][ROWS][AS_LD]  kernel rows of the chunk
+  double2* Xs = bsm + 2 * AS_ELEMS;  // [2][BT_KC][XS_LD] scaled sources of the chunk
   __shared__ double2* s_vec[N_SLOTS];
   __shared__ DevTask s_task;
   __shared__ DevTerm s_terms[BT_TERMS];
@@ -79,10 +87,10 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
   if (s_stop) return;
   const int m = a.m;
   const int kchunks = (m + BT_KC - 1) / BT_KC;
-  const int wr = (wid & 1) * 8;    // the warp's 8 output rows
-  const int wc = (wid >> 1) * 16;  // the warp's 16 output columns (two n-tiles)
+  const int wr = (wid % RG) * 8;         // the warp's 8 output rows
+  const int wc = (wid / RG) * (NT * 8);  // the warp's first output column
   const int kr = tid >> 4, xc = tid & 15;  // X staging: chunk row, columns xc + 16u
-  const int ar = tid / BT_KC, ak = tid % BT_KC;  // A staging: one 16-byte copy
+  const int ar = tid / BT_KC, ak = tid % BT_KC;  // A staging: one 16-byte copy (ar < ROWS)
   for (;;) {
     if (tid == 0) s_q = atomicAdd(a.head, 1);
     __syncthreads();
@@ -111,10 +119,13 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
     const int nch = nterm * kchunks;
 
     auto load_A = [&](int c, int buf) {
-      const int term = c / kchunks, kc = (c - term * kchunks) * BT_KC;
-      const double2* K = a.dense + ((size_t)s_terms[term].kernel * m + r0) * (size_t)m;
-      const bool ok = ar < nrows && kc + ak < m;
-      cp16z(As + buf * AS_ELEMS + ar * AS_LD + ak, ok ? K + (size_t)ar * m + kc + ak : K, ok ? 16 : 0);
+      if (ar < ROWS) {
+        const int term = c / kchunks, kc = (c - term * kchunks) * BT_KC;
+        const double2* K = a.dense + ((size_t)s_terms[term].kernel * m + r0) * (size_t)m;
+        const bool ok = ar < nrows && kc + ak < m;
+        cp16z(As + buf * AS_ELEMS + ar * AS_LD + ak, ok ? K + (size_t)ar * m + kc + ak : K,
+              ok ? 16 : 0);
+      }
       cp_commit();
     };
     double2 xa[4], xb[4];
@@ -142,9 +153,9 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
 #pragma unroll
       for (int u = 0; u < 4; ++u) d[16 * u] = cmul(sc, cadd(xa[u], xb[u]));
     };
-    double acc[2][2][2];  // [n-tile][re, im][pair]
+    double acc[NT][2][2];  // [n-tile][re, im][pair]
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < NT; ++u)
 #pragma unroll
       for (int v = 0; v < 2; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
     auto compute = [&](int buf) {
@@ -155,7 +166,7 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
         const double2 av = Ab[ks * 4];
         const double nai = -av.y;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < NT; ++u) {
           const double2 bv = Xb[ks * 4 * XS_LD + u * 8];
           dmma(acc[u][0], av.x, bv.x);
           dmma(acc[u][0], nai, bv.y);
@@ -189,7 +200,7 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
       const double2* rhsp = s_task.has_rhs ? s_vec[s_task.rhs.slot] + s_task.rhs.off * BW + rb : nullptr;
       const double rc = s_task.rhs_coef;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < NT; ++u) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = wc + 8 * u + 2 * (lane & 3) + e;
@@ -653,25 +664,34 @@ int elem_grid(int64_t n) {
 }  // namespace
 
 cudaError_t bexec_setup() {
-  cudaError_t e = cudaFuncSetAttribute(pt_bexec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)BEXEC_SMEM);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(pt_bexec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                              (int)cudaSharedmemCarveoutMaxShared);
+  for (const void* f : {(const void*)pt_bexec_kernel<16>, (const void*)pt_bexec_kernel<8>}) {
+    const int smem = (int)(f == (const void*)pt_bexec_kernel<16> ? bexec_smem<16>() : bexec_smem<8>());
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
-int bexec_grid(int device) {
+int bexec_grid(int device, int rows) {
   int nsm = 0, occ = 0;
   if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_bexec_kernel, BT_THREADS, BEXEC_SMEM) !=
-      cudaSuccess)
-    return 0;
+  cudaError_t e = rows == 8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_bexec_kernel<8>,
+                                                                            BT_THREADS, bexec_smem<8>())
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_bexec_kernel<16>,
+                                                                            BT_THREADS, bexec_smem<16>());
+  if (e != cudaSuccess) return 0;
   return nsm * std::max(occ, 1);
 }
 
-cudaError_t bexec_launch(const BExecArgs& a, int grid, cudaStream_t s) {
+cudaError_t bexec_launch(const BExecArgs& a, int grid, int rows, cudaStream_t s) {
   count_launch();
-  pt_bexec_kernel<<<grid, BT_THREADS, BEXEC_SMEM, s>>>(a);
+  if (rows == 8)
+    pt_bexec_kernel<8><<<grid, BT_THREADS, bexec_smem<8>(), s>>>(a);
+  else
+    pt_bexec_kernel<16><<<grid, BT_THREADS, bexec_smem<16>(), s>>>(a);
   return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@
 namespace pt {
 
 constexpr int BW = 64;           // right-hand sides per batch (columns)
-constexpr int BT_ROWS = 16;      // output rows of a batched task
+constexpr int BT_ROWS = 8;       // output rows of a batched task (8 or 16; PT_BATCH_ROWS; 8 measured faster at c5)
 constexpr int BT_KC = 16;        // kernel columns per staged chunk
 constexpr int BT_THREADS = 256;  // 8 warps: 2 row groups x 4 column groups
 constexpr int BT_TERMS = 16;     // kernel terms of one task
@@ -62,8 +62,8 @@ struct BGmresDev {
 };
 
 // one batched program launch (persistent, grid = bexec_grid())
-cudaError_t bexec_launch(const BExecArgs& a, int grid, cudaStream_t s);
-int bexec_grid(int device);
+cudaError_t bexec_launch(const BExecArgs& a, int grid, int rows, cudaStream_t s);
+int bexec_grid(int device, int rows);
 cudaError_t bexec_setup();
 
 // batched GMRES steps (graph-capturable; see pt_batch.cu)
