@@ -1,6 +1,6 @@
 """Launch one operator program a few times (ncu target; profiling aid).
 
-    python tools/ncu_target.py c3 A [reps] [max_iter]   # kinds: A, M, AM, G (GMRES)
+    python tools/ncu_target.py c3 A [reps] [max_iter]   # kinds: A, M, AM, G (GMRES), B (batched GMRES)
 """
 import sys
 from pathlib import Path
@@ -26,6 +26,9 @@ for _ in range(reps):
         op.apply_M(x, out=y)
     elif kind == "AM":
         op.apply_AM(x, out=y)
+    elif kind == "B":  # all recorded sources in lockstep (PT_GRAPH=0 for ncu)
+        op.gmres_batch(np.asarray(arr["rhs"]), rel_tol=1e-9,
+                       max_iter=int(sys.argv[4]) if len(sys.argv) > 4 else 2)
     else:
         op.gmres(torch.from_numpy(np.array(arr["rhs"][0])).cuda(), rel_tol=1e-9,
                  max_iter=int(sys.argv[4]) if len(sys.argv) > 4 else 2)
