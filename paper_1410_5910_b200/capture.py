@@ -86,7 +86,17 @@ def capture_operator(pol, perm, check=True):
         off = 0
         for k_id, sf in enumerate(kernels):
             if isinstance(sf, np.ndarray):
-                raise ValueError("mixed dense and compressed kernels are not supported")
+                # a dense kernel next to compressed ones (the extrapolation
+                # variant's E blocks, trace_system.py:460-464, are never
+                # compressed): one full leaf U = K, Vt = I; the reference
+                # reads its m x m entries
+                k_arr = np.asarray(sf, dtype=np.complex128)
+                leaf_rows.append((k_id, 0, 0, m, m, m, off, off + m * m))
+                chunks.append(np.ascontiguousarray(k_arr).ravel())
+                chunks.append(np.eye(m, dtype=np.complex128).ravel())
+                off += 2 * m * m
+                kbytes.append(16 * m * m)
+                continue
             leaves = leaves_from_sparse_form(sf)
             nb = 0
             for (r0, c0, u, vt) in leaves:

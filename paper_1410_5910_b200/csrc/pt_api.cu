@@ -308,6 +308,19 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
       op.kernel_bytes[k] += 16 * L.rank * (L.rows + L.cols);  // the reference's bytes
       if (L.rank > 0) kl.push_back(&L);
     }
+    // a dense kernel carried as one full leaf with Vt = I (mixed operators,
+    // e.g. the dense E blocks of the extrapolation variant next to compressed
+    // Green's blocks): the reference reads its m x m entries
+    if (kl.size() == 1 && kl[0]->row_off == 0 && kl[0]->col_off == 0 && kl[0]->rows == m &&
+        kl[0]->cols == m && kl[0]->rank == m) {
+      bool eye = true;
+      for (int64_t r = 0; r < m && eye; ++r)
+        for (int64_t c = 0; c < m && eye; ++c) {
+          const double* z = fac + 2 * (kl[0]->vt_off + r * m + c);
+          eye = z[0] == (r == c ? 1.0 : 0.0) && z[1] == 0.0;
+        }
+      if (eye) op.kernel_bytes[k] = 16 * m * m;
+    }
     // leaves whose factors outweigh their product are stored as the product
     // U.Vt (FP64, the same matrix to rounding): fewer bytes, and no T work
     auto dense_leaf = [&](const pt_leaf* L) {

@@ -28,7 +28,7 @@ from pathlib import Path
 import numpy as np
 
 from ..cache import read_case, write_case
-from .assemble import polarized_rhs, polarized_table
+from .assemble import extrapolator, extrapolator_pairs, polarized_rhs, polarized_table
 from .compress import leaf_table, plr_leaves
 from .configs import config
 from .layers import Layer, edge_extend, equal_partition
@@ -53,9 +53,13 @@ def _layer_job(job):
     blocks = lay.greens(job["pairs"])
     t2 = time.perf_counter()
     out = {}
-    for (j, k), blk in blocks.items():
+    for (j, k) in job["kernel_pairs"]:
+        blk = blocks[(j, k)]
         out[(j, k)] = blk if job["compression"] is None else \
             plr_leaves(blk, r_max=job["compression"][1], eps=job["compression"][0])
+    for d in job["extrapolators"]:  # dense, never compressed (trace_system.py:460-464)
+        num, den = extrapolator_pairs(job["n_layer"], d)
+        out[("E", d)] = extrapolator(blocks[num], blocks[den])
     t3 = time.perf_counter()
     newtons = [lay.newton(f) for f in job["f_local"]]
     if limiter is not None:
@@ -73,7 +77,8 @@ def build_operator(name, workers=None, sources=True):
     g, L = cfg.geo, cfg.L
     n_c = equal_partition(g.nz, L)
     m_ext = edge_extend(1.0 / cfg.c**2, g.n_pml)
-    entries, coefs, keys, perm = polarized_table(n_c, g.h)
+    variant = cfg.variant
+    entries, coefs, keys, perm = polarized_table(n_c, g.h, variant)
     jobs = []
     for ell in range(1, L + 1):
         lo = g.n_pml + n_c[ell - 1]
@@ -85,10 +90,15 @@ def build_operator(name, workers=None, sources=True):
                 fl = np.zeros((n_layer + 2 * g.n_pml, g.nx_ext), dtype=np.complex128)
                 fl[g.n_pml:g.n_pml + n_layer, :] = f[lo:lo + n_layer, :]
                 f_local.append(fl)
+        kpairs = sorted({(j, k) for (l_, j, k) in keys if l_ == ell and j != "E"}) \
+            if kernels_needed else []
+        extr = sorted({k for (l_, j, k) in keys if l_ == ell and j == "E"}) if kernels_needed else []
+        need = set(kpairs)
+        for d in extr:
+            need |= set(extrapolator_pairs(n_layer, d))
         jobs.append({"ell": ell, "nx": g.nx, "n_layer": n_layer, "h": g.h, "n_pml": g.n_pml,
                      "omega": float(cfg.omega), "m_tilde": edge_extend(rows, g.n_pml, axis=0),
-                     "pairs": sorted({(j, k) for (l_, j, k) in keys if l_ == ell})
-                     if kernels_needed else [],
+                     "pairs": sorted(need), "kernel_pairs": kpairs, "extrapolators": extr,
                      "compression": cfg.compression, "f_local": f_local})
     workers = workers or min(L, os.cpu_count() or 1)
     t0 = time.perf_counter()
@@ -105,7 +115,7 @@ def build_operator(name, workers=None, sources=True):
     meta = {"name": name, "note": cfg.note, "nx": g.nx, "nz": g.nz, "n_pml": g.n_pml, "h": g.h,
             "L": L, "n_c": [int(v) for v in n_c], "omega": float(cfg.omega), "m": g.nx_ext,
             "nt": 2 * L - 2, "N": 2 * (2 * L - 2) * g.nx_ext, "c_min": float(cfg.c.min()),
-            "c_max": float(cfg.c.max()), "variant": "jump", "gmres_tol": cfg.tol,
+            "c_max": float(cfg.c.max()), "variant": variant, "gmres_tol": cfg.tol,
             "gmres_max_iter": 100, "n_it": 2, "n_kernels": len(keys),
             "kernel_keys": [list(k) for k in keys],
             "compression": None if cfg.compression is None else
@@ -118,7 +128,7 @@ def build_operator(name, workers=None, sources=True):
         meta["operator_case"] = OPERATOR_OF[name]
         del arrays["entries"], arrays["coefs"], arrays["perm"]
     elif cfg.compression is None:
-        kernels = [per_layer[ell][0][(j, k)] for (ell, j, k) in keys]
+        kernels = [per_layer[ell][0][(j, k)] for (ell, j, k) in keys]  # (E, dir) for extrapolators
         meta["kernel_format"] = "dense"
         arrays["dense"] = np.stack(kernels)
         kb = np.full(len(keys), 16 * g.nx_ext**2, dtype=np.int64)
@@ -130,7 +140,7 @@ def build_operator(name, workers=None, sources=True):
         arrays["kernel_bytes"] = kb
         meta["kernel_bytes"] = int(kb.sum())
     if sources:
-        rhs = [polarized_rhs([per_layer[ell][1][s] for ell in range(1, L + 1)], n_c)
+        rhs = [polarized_rhs([per_layer[ell][1][s] for ell in range(1, L + 1)], n_c, variant)
                for s in range(len(cfg.sources))]
         arrays["rhs"] = np.stack(rhs)
         meta["source_labels"] = [lbl for lbl, _ in cfg.sources]

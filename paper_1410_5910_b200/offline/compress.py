@@ -48,10 +48,18 @@ def plr_leaves(block, r_max, eps):
 
 
 def leaf_table(kernels_leaves):
-    """Pack per-kernel leaf lists into the pt_leaf table + factor array."""
+    """Pack per-kernel leaf lists (or dense ndarrays) into the pt_leaf table + factor array."""
     rows, chunks, kbytes = [], [], []
     off = 0
     for kid, leaves in enumerate(kernels_leaves):
+        if isinstance(leaves, np.ndarray):  # a dense kernel: one full leaf U = K, Vt = I
+            m = leaves.shape[0]
+            rows.append((kid, 0, 0, m, m, m, off, off + m * m))
+            chunks.append(np.ascontiguousarray(leaves, dtype=np.complex128).ravel())
+            chunks.append(np.eye(m, dtype=np.complex128).ravel())
+            off += 2 * m * m
+            kbytes.append(16 * m * m)
+            continue
         nb = 0
         for (r0, c0, u, vt) in leaves:
             ml, r = u.shape

@@ -70,6 +70,7 @@ class CaseConfig:
     tol: float
     note: str
     extra: dict = field(default_factory=dict)
+    variant: str = "jump"    # polarized variant (trace_system.py:368-472)
 
 
 # ---- media -------------------------------------------------------------------
@@ -162,7 +163,7 @@ def source_random(g, seed):
 # ---- configurations ------------------------------------------------------------
 
 CASES = ["c1", "c2", "c3", "c3r", "c4", "c4r", "c5"]
-FIXTURES = ["fx_tiny", "fx_l2", "fx_uneven", "fx_plr", "fx_plr_odd"]
+FIXTURES = ["fx_tiny", "fx_l2", "fx_uneven", "fx_plr", "fx_plr_odd", "fx_extrap", "fx_extrap_plr"]
 
 
 def config(name: str) -> CaseConfig:
@@ -229,4 +230,16 @@ def config(name: str) -> CaseConfig:
                           [("point", source_point(g, 0.3, 0.5))], (1e-6, 3), 1e-10,
                           "PLR with odd m=53 (floor-first splits), eps 1e-6 (rank-deficient "
                           "leaves), L=3")
+    if name == "fx_extrap":
+        g = Geometry(30, 30, 10)
+        return CaseConfig(name, g, medium_homogeneous(g), 3, 9.0,
+                          [("point", source_point(g, 0.4, 0.6))], None, 1e-10,
+                          "extrapolation variant (reference test_solver.py pipeline geometry: 30^2, "
+                          "L=3, n_pml=10, omega=9, homogeneous), dense", variant="extrapolation")
+    if name == "fx_extrap_plr":
+        g = Geometry(40, 40, 10)
+        return CaseConfig(name, g, medium_gradient(g), 4, 9.0,
+                          [("point", source_point(g, 0.5, 0.25))], (1e-9, 4), 1e-10,
+                          "extrapolation variant with PLR Green's blocks and dense E blocks "
+                          "(mixed operator), m=60, r_max=4, L=4", variant="extrapolation")
     raise KeyError(f"unknown case {name!r}")

@@ -139,6 +139,25 @@ def test_reference_api_path(cuda_ok):
         S.solve_online(state, arr["rhs"][0], precond=S.PreconditionerConfig(variant="extrapolation"))
 
 
+@pytest.mark.parametrize("name", ["fx_extrap", "fx_extrap_plr"])
+def test_extrapolation_variant_api_path(cuda_ok, name):
+    """The extrapolation variant (trace_system.py:460-464; the reference pins it
+    end to end in test_solver.py:224-238): dense E blocks at scale 1.0, in the
+    PLR fixture next to compressed Green's blocks (a mixed operator)."""
+    from paper_1410_5910_b200 import solver as S
+    state = S.OfflineState.from_case(golden_path(name))
+    meta, arr = load_case_arrays(golden_path(name))
+    assert state.variant == "extrapolation"
+    pc = S.PreconditionerConfig(variant="extrapolation")
+    x, rep = S.solve_online(state, arr["rhs"][0], precond=pc,
+                            gmres=S.GmresConfig(rel_tol=meta["gmres_tol"]))
+    assert abs(rep.iterations - meta["solves"][0]["iterations"]) <= 1
+    assert rel(rep.traces, arr["ref_traces"][0]) <= TRACE_TOL
+    assert rel(x, arr["ref_x"][0]) <= TRACE_TOL
+    with pytest.raises(ValueError, match="variant"):
+        S.solve_online(state, arr["rhs"][0], precond=S.PreconditionerConfig())
+
+
 # ---- the reference's GMRES unit tests through the device Arnoldi/Givens path
 
 

@@ -38,7 +38,7 @@ def test_partition_remainder_to_front():
 @pytest.mark.parametrize("name", FIXTURES + ["c1_ref", "c3r_ref", "c2_ref", "c3_ref"])
 def test_entry_table_matches_reference(name):
     meta, arr = read_case(golden_path(name))
-    entries, coefs, keys, perm = polarized_table(meta["n_c"], meta["h"])
+    entries, coefs, keys, perm = polarized_table(meta["n_c"], meta["h"], meta.get("variant", "jump"))
     assert np.array_equal(entries, arr["entries"])
     assert np.array_equal(coefs, arr["coefs"])
     assert np.array_equal(perm, arr["perm"])

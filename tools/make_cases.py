@@ -71,7 +71,7 @@ def config(name):
     if c.compression is not None:
         comp = CompressionConfig(epsilon=c.compression[0], r_max=c.compression[1])
     return dict(grid=g, c=c.c, L=c.L, omega=c.omega, sources=c.sources, compression=comp,
-                tol=c.tol, note=c.note)
+                tol=c.tol, note=c.note, variant=c.variant)
 
 
 def model_from_c(grid, c):
@@ -103,8 +103,8 @@ def build(name, out_dir, operator_from=None, state_cache={}):
         state = state_cache[op_key]
         offline_s = None
     else:
-        state = offline_assemble(grid, model, part, omega, factor_method="sparse",
-                                 compression=cfg["compression"])
+        state = offline_assemble(grid, model, part, omega, variant=cfg["variant"],
+                                 factor_method="sparse", compression=cfg["compression"])
         offline_s = time.perf_counter() - t0
         state_cache[op_key] = state
     print(f"[{name}] offline {offline_s}s stages={state.stage_seconds}", flush=True)
@@ -151,10 +151,11 @@ def build(name, out_dir, operator_from=None, state_cache={}):
 
     # reference solves
     gm = GmresConfig(rel_tol=cfg["tol"])
+    pc = PreconditionerConfig(variant=cfg["variant"])
     rhs_list, x_list, tr_list, hist_list, recs = [], [], [], [], []
     u0 = None
     for s, (label, f) in enumerate(cfg["sources"]):
-        rep = solve_helmholtz(model, grid, part, f, state=state, gmres=gm)
+        rep = solve_helmholtz(model, grid, part, f, state=state, precond=pc, gmres=gm)
         # the polarized rhs the pipeline handed to GMRES, and its solution x
         from helmsweep.local_solver import newton_trace
         from helmsweep.partition import restrict_source
@@ -197,7 +198,7 @@ def build(name, out_dir, operator_from=None, state_cache={}):
     return out
 
 
-FIXTURES = ["fx_tiny", "fx_l2", "fx_uneven", "fx_plr", "fx_plr_odd"]
+from paper_1410_5910_b200.offline.configs import FIXTURES  # noqa: E402
 LITE_SUBSET = {"c5": list(range(0, 64, 9))}
 
 
