@@ -141,6 +141,7 @@ struct pt_handle {
   int64_t srun_cap = 0;    // dense-leaf source runs of a task (PLR)
   int64_t slot_bytes = 0;  // bytes of one task slot
   int n_stages = 4;        // operator ring stages
+  int n_slots = EXEC_TSLOTS;  // task slots in use per CTA
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
   int poll_stagger = 0;    // staggered polling of few counters (PT_POLL_STAGGER cycles; 0: off)
   std::unique_ptr<pt_gmres_ws> gws;
@@ -583,6 +584,7 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.src_cap = h->src_cap;
   a.slot_bytes = h->slot_bytes;
   a.n_stages = h->n_stages;
+  a.n_slots = h->n_slots;
   a.poll_ns = h->poll_ns;
   a.poll_stagger = h->poll_stagger;
   a.n_tasks = (int)p->host.tasks.size();
@@ -838,8 +840,8 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
       (h->src_cap + EXEC_EPI * EXEC_EPI_SRC + EXEC_TERMS + EXEC_EYES) * (int64_t)sizeof(double2) +
       EXEC_SRCS * (int64_t)sizeof(void*);
   h->slot_bytes = (h->slot_bytes + 127) / 128 * 128;
-  // + the consumers' partials
-  const size_t fixed = (size_t)EXEC_TSLOTS * h->slot_bytes + EXEC_CONSUMERS * sizeof(double2);
+  // + the consumers' partials (the slot count is settled below)
+  size_t fixed = (size_t)EXEC_TSLOTS * h->slot_bytes + EXEC_CONSUMERS * sizeof(double2);
   // B200 figures for a host-only handle; the device's own otherwise
   int smem_sm = 233472, smem_blk = 232448, reserved = 1024, nsm = 148;
   cudaFuncAttributes fa{};
@@ -851,7 +853,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     CK(cudaFuncGetAttributes(&fa, pt_exec_kernel));
     cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
   }
-  int target = 1;  // one CTA of EXEC_THREADS per SM
+  const int target = 512 / EXEC_CONSUMERS;  // CTAs of EXEC_THREADS per SM
   // ring: 3 stages (PT_STAGES overrides, 2..8; fewer if a stage would not
   // hold `need`).  Items address a stage with 16-bit offsets.
   int max_stages = 3;
@@ -859,15 +861,29 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     max_stages = std::max(2, std::min(EXEC_MAX_STAGES, std::atoi(e)));
   int64_t half = 0;
   int ctas_sm = 1, stages = 2;
-  for (int c = target; c >= 1 && half < need; --c) {
-    ctas_sm = c;
-    const int64_t per_cta =
-        std::min<int64_t>(smem_sm / c - reserved - (int64_t)fa.sharedSizeBytes - 128, smem_blk);
-    for (stages = max_stages; stages >= 2; --stages) {
-      const int64_t hb = (per_cta - (int64_t)fixed) / stages;
-      half = hb > 0 ? std::min<int64_t>(65528, (hb / (int64_t)sizeof(double2)) / 8 * 8) : 0;
-      if (half >= need) break;
+  // Task slots: as many as leave the ring stages room for a full task piece
+  // (DENSE_RT_MAX dense kernel rows, or 2048 PLR elements); fewer slots
+  // otherwise (big dense slots: c2 at three slots would stage one kernel row
+  // per piece).  PT_SLOTS overrides.
+  const int64_t want = op.fmt == PT_KERNEL_DENSE ? DENSE_RT_MAX * op.m : std::max<int64_t>(need, 2048);
+  int min_slots = 2, max_slots = EXEC_TSLOTS;
+  if (const char* e = std::getenv("PT_SLOTS"))
+    min_slots = max_slots = std::max(1, std::min(EXEC_TSLOTS, std::atoi(e)));
+  for (int ns = max_slots; ns >= min_slots; --ns) {
+    h->n_slots = ns;
+    fixed = (size_t)ns * h->slot_bytes + EXEC_CONSUMERS * sizeof(double2);
+    half = 0;
+    for (int c = target; c >= 1 && half < need; --c) {
+      ctas_sm = c;
+      const int64_t per_cta =
+          std::min<int64_t>(smem_sm / c - reserved - (int64_t)fa.sharedSizeBytes - 128, smem_blk);
+      for (stages = max_stages; stages >= 2; --stages) {
+        const int64_t hb = (per_cta - (int64_t)fixed) / stages;
+        half = hb > 0 ? std::min<int64_t>(65528, (hb / (int64_t)sizeof(double2)) / 8 * 8) : 0;
+        if (half >= need) break;
+      }
     }
+    if (half >= want) break;
   }
   if (half < need) return fail(PT_EINVAL, "block size too large for the executor's shared memory");
   h->pp.half_elems = half;

@@ -9,7 +9,10 @@ namespace pt {
 
 // executor CTA (one per SM): 16 consumer warps + 2 producer warps (one per
 // task slot)
-constexpr int EXEC_CONSUMERS = 512;
+#ifndef PT_EXEC_CONSUMERS
+#define PT_EXEC_CONSUMERS 512
+#endif
+constexpr int EXEC_CONSUMERS = PT_EXEC_CONSUMERS;  // 512: one CTA per SM; 256: two
 #ifndef PT_EXEC_PRODUCERS
 #define PT_EXEC_PRODUCERS 3
 #endif
@@ -111,6 +114,7 @@ struct ExecArgs {
   int64_t blob_cap;          // bytes of a task slot's blob area
   int64_t slot_bytes;        // bytes of one task slot
   int32_t n_stages;          // ring stages (<= EXEC_MAX_STAGES)
+  int32_t n_slots;           // task slots in use (2..EXEC_TSLOTS)
   int32_t poll_ns;           // back-off between dependency polls (0: spin)
   int32_t poll_stagger;      // cycles between the staggered lanes' first polls (0: off)
   const int* stop;  // GMRES status stop flag: the whole launch is skipped once set

@@ -159,6 +159,7 @@ struct Layout {
   char* base;
   int64_t stage_bytes, slot_bytes, blob_cap, vec_cap;
   int n_stages;
+  int n_slots;  // task slots in use (<= EXEC_TSLOTS)
   __device__ __forceinline__ double2* stage(int s) const {
     return reinterpret_cast<double2*>(base + (size_t)s * stage_bytes);
   }
@@ -178,7 +179,7 @@ struct Layout {
   }
   __device__ __forceinline__ double2* part() const {
     return reinterpret_cast<double2*>(base + (size_t)n_stages * stage_bytes +
-                                      EXEC_TSLOTS * (size_t)slot_bytes);
+                                      (size_t)n_slots * (size_t)slot_bytes);
   }
 };
 
@@ -190,6 +191,7 @@ __device__ __forceinline__ Layout carve(double2* base, const ExecArgs& a) {
   L.blob_cap = a.blob_cap;
   L.vec_cap = a.src_cap;
   L.n_stages = a.n_stages;
+  L.n_slots = a.n_slots;
   return L;
 }
 
@@ -341,7 +343,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
   const Slot sl = L.slot(k);
   int n_staged = 0;  // phases of this slot's staging barrier
   for (int j = 0;; ++j) {
-    const int use = EXEC_TSLOTS * j + k;
+    const int use = L.n_slots * j + k;
     if (j > 0) {  // consumers done with use - 2: publish its outputs
       bar_wait(&s_tempty[k], (j - 1) & 1);
       if (lane == 0) {  // release: the consumers' outputs before the count
@@ -602,9 +604,9 @@ __device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t,
 __device__ void consumer(const ExecArgs& a, const Layout& L) {
   Ring rg{0, 0u};  // pieces consumed
   for (int use = 0;; ++use) {
-    const int k = use % EXEC_TSLOTS;
+    const int k = use % L.n_slots;
     const Slot sl = L.slot(k);
-    bar_wait(&s_tfull[k], (use / EXEC_TSLOTS) & 1);  // acquire the producer's staging
+    bar_wait(&s_tfull[k], (use / L.n_slots) & 1);  // acquire the producer's staging
     const DevTask& t = sl.desc();
     if (t.type < 0) return;
     const int q = t.q;
@@ -633,7 +635,7 @@ __device__ void consumer(const ExecArgs& a, const Layout& L) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(EXEC_THREADS, 1) pt_exec_kernel(ExecArgs a) {
+__global__ void __launch_bounds__(EXEC_THREADS, 512 / EXEC_CONSUMERS) pt_exec_kernel(ExecArgs a) {
   extern __shared__ __align__(128) double2 smem[];
   __shared__ int s_stop;
   if (a.stop) {
@@ -669,10 +671,12 @@ __global__ void __launch_bounds__(EXEC_THREADS, 1) pt_exec_kernel(ExecArgs a) {
   }
   __syncthreads();
   const Layout L = carve(smem, a);
-  if (threadIdx.x >= CONSUMERS)
-    producer(a, L, (threadIdx.x - CONSUMERS) >> 5);
-  else
+  if (threadIdx.x >= CONSUMERS) {
+    const int k = (threadIdx.x - CONSUMERS) >> 5;
+    if (k < L.n_slots) producer(a, L, k);  // unused task slots: their warps retire
+  } else {
     consumer(a, L);
+  }
 }
 
 }  // namespace pt
