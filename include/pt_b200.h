@@ -233,6 +233,53 @@ int pt_plan_stats(pt_handle *h, int32_t kind, int32_t n_it, int64_t *stats);
 int pt_plan_tasks(pt_handle *h, int32_t kind, int32_t n_it, int32_t *rec,
                   int64_t cap, int64_t *n_out);
 
+/* ---- per-layer local solves (Newton traces, volume reconstruction) --------
+ * The reference solves each layer's sparse system with SuperLU on the host
+ * (LocalFactorization.solve, local_solver.py:21-60) for the Newton traces
+ * (newton_trace, :138-144) and the volume (reconstruct_volume, :147-176).
+ * Here the host offline stage factors every layer once (Pr (P A P^T) Pc = L U
+ * with a nested-dissection P) and these calls keep L and U of all layers on
+ * the device and solve every layer in one pass of two sync-free sparse
+ * triangular solves.  Per layer: CSR of L and U (complex values interleaved,
+ * diagonal included) and the composed gathers q_in (y[k] = b[q_in[k]], b in
+ * the layer's natural (z, x) order) and q_out (x[r] = z[q_out[r]]). */
+typedef struct pt_local pt_local;
+typedef struct {
+  int64_t dim;                 /* nze * nxe unknowns of the layer           */
+  int64_t nze, nxe;            /* layer grid incl. the z pads (local_solver) */
+  int64_t n_layer, n_pml;      /* interior rows, pad rows on each side      */
+  const int64_t *l_ptr;        /* dim + 1 */
+  const int32_t *l_col;
+  const double *l_val;         /* complex */
+  const int64_t *u_ptr;
+  const int32_t *u_col;
+  const double *u_val;
+  const int64_t *q_in, *q_out; /* dim each, layer-local indices */
+} pt_local_layer;
+/* layers in depth order (layer l's interior rows follow layer l-1's) */
+int pt_local_create(const pt_local_layer *layers, int32_t n_layers, int device,
+                    pt_local **out);
+int pt_local_destroy(pt_local *h);
+/* rows = total unknowns, factor_nnz = stored entries of L and U, levels =
+ * dependency depth of the triangular solves */
+int pt_local_info(const pt_local *h, int64_t *rows, int64_t *factor_nnz,
+                  int32_t *l_levels, int32_t *u_levels);
+/* x = H^-1 b for every layer (layers concatenated, natural order; device) */
+int pt_local_solve(pt_local *h, const double *b, double *x, pt_stream stream);
+/* Newton traces of source f (extended grid, nz_ext x nxe, device):
+ * traces[l][d][c] at local depths d = (0, 1, n, n+1) (newton_trace) and/or
+ * the polarized right-hand side (polarized_rhs, trace_system.py:475-484;
+ * jump = 0: the extrapolation variant's zero bottom half).  Either output
+ * may be NULL (not both). */
+int pt_local_newton(pt_local *h, const double *f, double *traces, double *rhs,
+                    int32_t jump, pt_stream stream);
+/* Volume of every layer (reconstruct_volume with the interface forcing of
+ * the traces x_down + x_up of the GMRES solution x; solver.py:403-426):
+ * u (nz x nxe interior rows, device). */
+int pt_local_reconstruct(pt_local *h, const double *f, const double *x,
+                         double h_step, double *u, pt_stream stream);
+const char *pt_local_last_error(void);
+
 /* ---- misc ----------------------------------------------------------------*/
 const char *pt_last_error(void);
 int32_t pt_abi_version(void);

@@ -48,6 +48,14 @@ class Report(C.Structure):
                 ("residual_history", C.POINTER(C.c_double))]
 
 
+class LocalLayer(C.Structure):
+    _fields_ = [("dim", C.c_int64), ("nze", C.c_int64), ("nxe", C.c_int64),
+                ("n_layer", C.c_int64), ("n_pml", C.c_int64),
+                ("l_ptr", C.c_void_p), ("l_col", C.c_void_p), ("l_val", C.c_void_p),
+                ("u_ptr", C.c_void_p), ("u_col", C.c_void_p), ("u_val", C.c_void_p),
+                ("q_in", C.c_void_p), ("q_out", C.c_void_p)]
+
+
 _VP = C.c_void_p
 _SIGS = {
     "pt_create": (C.c_int, [C.POINTER(Layout), C.POINTER(Entry), C.c_int64, C.POINTER(C.c_int64),
@@ -83,6 +91,14 @@ _SIGS = {
                                C.POINTER(C.c_int64)]),
     "pt_exec_info": (C.c_int, [_VP, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64)]),
+    "pt_local_create": (C.c_int, [C.POINTER(LocalLayer), C.c_int32, C.c_int, C.POINTER(_VP)]),
+    "pt_local_destroy": (C.c_int, [_VP]),
+    "pt_local_info": (C.c_int, [_VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "pt_local_solve": (C.c_int, [_VP, _VP, _VP, _VP]),
+    "pt_local_newton": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int32, _VP]),
+    "pt_local_reconstruct": (C.c_int, [_VP, _VP, _VP, C.c_double, _VP, _VP]),
+    "pt_local_last_error": (C.c_char_p, []),
     "pt_last_error": (C.c_char_p, []),
     "pt_abi_version": (C.c_int32, []),
     "pt_launch_count": (C.c_int64, []),

@@ -1,0 +1,503 @@
+// Per-layer local solves on the device: Newton traces and volume
+// reconstruction.
+//
+// The reference solves every layer's sparse system with SuperLU on the host
+// (LocalFactorization.solve, local_solver.py:21-60) twice per source: once for
+// the Newton traces (newton_trace, :138-144) and once for the volume
+// (reconstruct_volume, :147-176).  Here the host offline stage factors each
+// layer once (offline/local.py: geometric nested-dissection order, SuperLU
+// with that order), and the device keeps L and U of ALL layers resident and
+// solves them together:
+//
+//   y = b[q_in]   (the layer's right-hand side, gathered through the composed
+//                  row / nested-dissection permutation)
+//   L w = y, U z = w   (sparse triangular solves)
+//   x = z[q_out]  (back to the layer's natural (z, x) grid order)
+//
+// Triangular solves are "sync-free": one warp per row, rows handed out from a
+// queue sorted by dependency level across all layers (so the layers advance
+// together), each warp spins on the flags of the rows its row depends on and
+// publishes its own value with a release flag.  One launch per triangular
+// factor for every layer; no grid barrier.  Flags carry an epoch, so no reset
+// between solves.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pt_b200.h"
+#include "pt_device.cuh"
+
+namespace pt {
+extern void count_launch();
+}
+using namespace pt;
+
+namespace {
+
+thread_local std::string g_lerr;
+int lfail(int code, const std::string& m) {
+  g_lerr = m;
+  return code;
+}
+#define LCK(x)                                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) return lfail(PT_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct LayerDev {
+  int64_t row0;     // first global row of the layer's unknowns
+  int64_t dim;      // nze * nxe
+  int32_t nze, nxe, n_layer, n_pml;
+  int64_t f_row0;   // extended-grid row of the layer's depth 1
+  int64_t u_row0;   // first interior row of the layer in the volume output
+  int32_t has_top, has_bot;  // interface above (l >= 2) / below (l <= L-1)
+  int32_t top, bot;          // trace blocks 2(l-2) and 2(l-1)
+};
+
+// ---- sync-free sparse triangular solve (one warp per row) -------------------
+__global__ void __launch_bounds__(1024)
+k_trsv(const int* __restrict__ order, int n, const int64_t* __restrict__ ptr,
+       const int* __restrict__ col, const double2* __restrict__ val, const double2* __restrict__ dinv,
+       const double2* b, double2* x, int* flag, int epoch, int* head) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int q = 0;
+    if (lane == 0) q = atomicAdd(head, 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    if (q >= n) return;
+    const int i = __ldg(order + q);
+    const int64_t e0 = __ldg(ptr + i), e1 = __ldg(ptr + i + 1);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int j = __ldg(col + e);
+      while (ld_acquire(flag + j) != epoch) {
+      }
+      acc = cfma(__ldg(val + e), ld_cg(x + j), acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double2 r = csub(ld_cg(b + i), acc);
+      st_cg(x + i, cmul(r, __ldg(dinv + i)));
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag + i), "r"(epoch) : "memory");
+    }
+  }
+}
+
+// y[G] = b_layer[q_in[k]] for every global row G = row0 + k.  b_layer is the
+// layer's forcing in natural (z, x) order: f restricted to the layer rows
+// (restrict_source, partition.py:104-113) plus, when x_traces is given, the
+// interface forcing of reconstruct_volume (local_solver.py:160-173) from the
+// GMRES solution x (traces = x_down + x_up, block order a_1, b_1, ...).
+__global__ void k_gather_rhs(const LayerDev* __restrict__ lay, int n_layers, const int64_t* q_in,
+                             int64_t total, const double2* f, const double2* xsol, int64_t nt_m,
+                             double w, double2* y) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (l + 1 < n_layers && lay[l + 1].row0 <= g) ++l;
+    const LayerDev& L = lay[l];
+    const int64_t idx = q_in[g];
+    const int r = (int)(idx / L.nxe), c = (int)(idx % L.nxe);
+    double2 v = make_double2(0.0, 0.0);
+    if (r >= L.n_pml && r < L.n_pml + L.n_layer) v = f[(L.f_row0 + r - L.n_pml) * L.nxe + c];
+    if (xsol) {
+      auto tr = [&](int blk) {  // trace block blk, column c
+        const int64_t o = (int64_t)blk * L.nxe + c;
+        return cadd(xsol[o], xsol[nt_m + o]);
+      };
+      const int d0 = L.n_pml - 1, d1 = L.n_pml, dn = L.n_pml + L.n_layer - 1, dn1 = L.n_pml + L.n_layer;
+      if (L.has_top) {
+        if (r == d1) v = cadd(v, make_double2(w * tr(L.top).x, w * tr(L.top).y));           // + w u0
+        if (r == d0) v = csub(v, make_double2(w * tr(L.top + 1).x, w * tr(L.top + 1).y));   // - w u1
+      }
+      if (L.has_bot) {
+        if (r == dn1) v = csub(v, make_double2(w * tr(L.bot).x, w * tr(L.bot).y));         // - w un
+        if (r == dn) v = cadd(v, make_double2(w * tr(L.bot + 1).x, w * tr(L.bot + 1).y));  // + w un1
+      }
+    }
+    y[g] = v;
+  }
+}
+
+// Newton traces: out[l][d][c] = x_l at local depth (0, 1, n, n+1)[d], column c
+__global__ void k_newton_out(const LayerDev* __restrict__ lay, int n_layers, const int64_t* q_out,
+                             const double2* z, double2* out) {
+  const int l = blockIdx.y, d = blockIdx.z;
+  const LayerDev& L = lay[l];
+  const int depth = d == 0 ? 0 : d == 1 ? 1 : d == 2 ? L.n_layer : L.n_layer + 1;
+  const int r = L.n_pml + depth - 1;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.nxe; c += gridDim.x * blockDim.x)
+    out[((int64_t)l * 4 + d) * L.nxe + c] = z[L.row0 + q_out[L.row0 + (int64_t)r * L.nxe + c]];
+}
+
+// polarized rhs (trace_system.py:475-484) from the Newton traces:
+// top = -[N^i(n_i), N^{i+1}(1)]_i, bottom = -[N^i(n_i + 1), N^{i+1}(0)]_i (jump)
+// or 0 (extrapolation)
+__global__ void k_polarized_rhs(const double2* nw, int n_layers, int nxe, int64_t nt_m, int jump,
+                                double2* rhs) {
+  const int64_t total = 2 * nt_m;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const bool bottom = e >= nt_m;
+    const int64_t o = bottom ? e - nt_m : e;
+    const int blk = (int)(o / nxe), c = (int)(o % nxe);
+    const int i = blk / 2 + 1;  // interface 1..L-1
+    double2 v = make_double2(0.0, 0.0);
+    if (!bottom || jump) {
+      // block 2(i-1): layer i at depth n (top) / n+1 (bottom): slots 2 / 3
+      // block 2i-1:   layer i+1 at depth 1 (top) / 0 (bottom): slots 1 / 0
+      const int l = (blk % 2 == 0) ? i - 1 : i;
+      const int slot = (blk % 2 == 0) ? (bottom ? 3 : 2) : (bottom ? 0 : 1);
+      const double2 u = nw[((int64_t)l * 4 + slot) * nxe + c];
+      v = make_double2(-u.x, -u.y);
+    }
+    rhs[e] = v;
+  }
+}
+
+// volume: u[(u_row0 + r) * nxe + c] = x_l at layer row n_pml + r, r < n_layer
+__global__ void k_volume_out(const LayerDev* __restrict__ lay, int n_layers, const int64_t* q_out,
+                             const double2* z, double2* u) {
+  const int l = blockIdx.y;
+  const LayerDev& L = lay[l];
+  const int64_t n = (int64_t)L.n_layer * L.nxe;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / L.nxe, c = e % L.nxe;
+    u[(L.u_row0 + r) * L.nxe + c] = z[L.row0 + q_out[L.row0 + (L.n_pml + r) * L.nxe + c]];
+  }
+}
+
+// dst[g] = src[row0(layer of g) + q[g]]  (q layer-local)
+__global__ void k_gather(const int64_t* __restrict__ q, const LayerDev* __restrict__ lay, int nl,
+                         int64_t n, const double2* src, double2* dst) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (l + 1 < nl && lay[l + 1].row0 <= g) ++l;
+    dst[g] = src[lay[l].row0 + q[g]];
+  }
+}
+
+int elem_grid(int64_t n) { return (int)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 4096); }
+
+}  // namespace
+
+struct pt_local {
+  int device = 0;
+  int n_layers = 0;
+  int64_t rows = 0;   // total unknowns over the layers
+  int64_t nz = 0;     // interior rows of the volume
+  int64_t nxe = 0;
+  std::vector<LayerDev> host_layers;
+  LayerDev* layers = nullptr;
+  // factors (global row / column indices), off-diagonal CSR + 1/diagonal
+  int64_t *l_ptr = nullptr, *u_ptr = nullptr;
+  int *l_col = nullptr, *u_col = nullptr;
+  double2 *l_val = nullptr, *u_val = nullptr, *l_dinv = nullptr, *u_dinv = nullptr;
+  int *l_order = nullptr, *u_order = nullptr;
+  int64_t *q_in = nullptr, *q_out = nullptr;
+  double2 *y = nullptr, *w = nullptr, *z = nullptr;
+  double2* newton = nullptr;  // Newton traces scratch (n_layers x 4 x nxe)
+  int* flag = nullptr;  // [rows] for L, [rows] for U
+  int* head = nullptr;  // queue heads (2 per solve)
+  int epoch = 0;
+  int grid = 0;
+  int64_t factor_nnz = 0;
+  int32_t l_levels = 0, u_levels = 0;
+  ~pt_local() {
+    for (void* p : {(void*)layers, (void*)l_ptr, (void*)u_ptr, (void*)l_col, (void*)u_col,
+                    (void*)l_val, (void*)u_val, (void*)l_dinv, (void*)u_dinv, (void*)l_order,
+                    (void*)u_order, (void*)q_in, (void*)q_out, (void*)y, (void*)w, (void*)z, (void*)newton,
+                    (void*)flag, (void*)head})
+      cudaFree(p);
+  }
+};
+
+namespace {
+
+template <class T>
+int up(T** dst, const std::vector<T>& v) {
+  *dst = nullptr;
+  if (v.empty()) return 0;
+  LCK(cudaMalloc((void**)dst, v.size() * sizeof(T)));
+  LCK(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+// Split one layer's CSR factor (rows of the permuted system, complex values)
+// into off-diagonal entries (global columns) and 1/diagonal; dependency
+// levels (lower: rows ascending; upper: descending).
+int split_factor(const int64_t* ptr, const int32_t* col, const double* val, int64_t dim,
+                 int64_t row0, bool lower, std::vector<int64_t>& gptr, std::vector<int>& gcol,
+                 std::vector<double2>& gval, std::vector<double2>& dinv, std::vector<int>& level) {
+  std::vector<int> lv(dim, 0);
+  std::vector<double2> d(dim, make_double2(0.0, 0.0));
+  std::vector<char> has(dim, 0);
+  // off-diagonals (and levels, which need rows in dependency order)
+  const int64_t base = (int64_t)gcol.size();
+  (void)base;
+  for (int64_t r = 0; r < dim; ++r) {
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+      const int64_t c = col[e];
+      if (c < 0 || c >= dim) return lfail(PT_EINVAL, "local factor column out of range");
+      if (c == r) {
+        d[r] = make_double2(val[2 * e], val[2 * e + 1]);
+        has[r] = 1;
+      } else if ((c < r) != lower) {
+        return lfail(PT_EINVAL, lower ? "L factor has entries above the diagonal"
+                                      : "U factor has entries below the diagonal");
+      }
+    }
+  }
+  for (int64_t k = 0; k < dim; ++k) {
+    const int64_t r = lower ? k : dim - 1 - k;
+    int m = 0;
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e)
+      if (col[e] != r) m = std::max(m, lv[col[e]] + 1);
+    lv[r] = m;
+  }
+  for (int64_t r = 0; r < dim; ++r) {
+    if (!has[r] || (d[r].x == 0.0 && d[r].y == 0.0))
+      return lfail(PT_EINVAL, "local factor has a zero or missing diagonal");
+    const double dd = d[r].x * d[r].x + d[r].y * d[r].y;
+    dinv.push_back(make_double2(d[r].x / dd, -d[r].y / dd));
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e)
+      if (col[e] != r) {
+        gcol.push_back((int)(row0 + col[e]));
+        gval.push_back(make_double2(val[2 * e], val[2 * e + 1]));
+      }
+    gptr.push_back((int64_t)gcol.size());
+    level.push_back(lv[r]);
+  }
+  return 0;
+}
+
+std::vector<int> level_order(const std::vector<int>& level, int32_t* nlev) {
+  const int n = (int)level.size();
+  int mx = 0;
+  for (int v : level) mx = std::max(mx, v);
+  *nlev = mx + 1;
+  std::vector<int> cnt(mx + 2, 0), order(n);
+  for (int v : level) cnt[v + 1]++;
+  for (int v = 0; v <= mx; ++v) cnt[v + 1] += cnt[v];
+  for (int i = 0; i < n; ++i) order[cnt[level[i]]++] = i;  // stable: layers interleave per level
+  return order;
+}
+
+int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) {
+  const int e = h->epoch;
+  count_launch();
+  k_trsv<<<h->grid, 1024, 0, s>>>(lower ? h->l_order : h->u_order, (int)h->rows,
+                                  lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col,
+                                  lower ? h->l_val : h->u_val, lower ? h->l_dinv : h->u_dinv, b, x,
+                                  h->flag + (lower ? 0 : h->rows), e, h->head + (lower ? 0 : 1));
+  LCK(cudaGetLastError());
+  return 0;
+}
+
+// b -> z for every layer: L w = y (y gathered by the caller), U z = w
+int solve_all(pt_local* h, cudaStream_t s) {
+  ++h->epoch;
+  LCK(cudaMemsetAsync(h->head, 0, 2 * sizeof(int), s));
+  int rc;
+  if ((rc = trsv(h, true, h->y, h->w, s))) return rc;
+  return trsv(h, false, h->w, h->z, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pt_local_last_error(void) { return g_lerr.c_str(); }
+
+int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, pt_local** out) {
+  if (!layers || n_layers < 1 || !out) return lfail(PT_EINVAL, "bad arguments to pt_local_create");
+  *out = nullptr;
+  int ndev = 0;
+  LCK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return lfail(PT_EINVAL, "no such CUDA device");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  std::unique_ptr<pt_local> h(new pt_local());
+  h->device = device;
+  h->n_layers = n_layers;
+  std::vector<int64_t> lptr{0}, uptr{0}, qin, qout;
+  std::vector<int> lcol, ucol, llev, ulev;
+  std::vector<double2> lval, uval, ldinv, udinv;
+  int64_t row0 = 0, u_row0 = 0;
+  const int64_t nxe = layers[0].nxe;
+  for (int l = 0; l < n_layers; ++l) {
+    const pt_local_layer& A = layers[l];
+    if (A.nxe != nxe || A.nze < 1 || A.n_layer < 1 || A.n_pml < 1 || A.dim != A.nze * A.nxe ||
+        A.nze != A.n_layer + 2 * A.n_pml || !A.l_ptr || !A.u_ptr || !A.q_in || !A.q_out)
+      return lfail(PT_EINVAL, "inconsistent local layer geometry");
+    LayerDev d{};
+    d.row0 = row0;
+    d.dim = A.dim;
+    d.nze = (int32_t)A.nze;
+    d.nxe = (int32_t)A.nxe;
+    d.n_layer = (int32_t)A.n_layer;
+    d.n_pml = (int32_t)A.n_pml;
+    d.f_row0 = A.n_pml + u_row0;  // extended-grid row of the layer's depth 1
+    d.u_row0 = u_row0;
+    d.has_top = l >= 1;
+    d.has_bot = l <= n_layers - 2;
+    d.top = 2 * (l - 1);
+    d.bot = 2 * l;
+    h->host_layers.push_back(d);
+    int rc;
+    if ((rc = split_factor(A.l_ptr, A.l_col, A.l_val, A.dim, row0, true, lptr, lcol, lval, ldinv, llev)))
+      return rc;
+    if ((rc = split_factor(A.u_ptr, A.u_col, A.u_val, A.dim, row0, false, uptr, ucol, uval, udinv, ulev)))
+      return rc;
+    for (int64_t k = 0; k < A.dim; ++k) {
+      if (A.q_in[k] < 0 || A.q_in[k] >= A.dim || A.q_out[k] < 0 || A.q_out[k] >= A.dim)
+        return lfail(PT_EINVAL, "local permutation out of range");
+      qin.push_back(A.q_in[k]);
+      qout.push_back(A.q_out[k]);
+    }
+    row0 += A.dim;
+    u_row0 += A.n_layer;
+  }
+  if (row0 > INT32_MAX) return lfail(PT_EINVAL, "too many local unknowns");
+  h->rows = row0;
+  h->nz = u_row0;
+  h->nxe = nxe;
+  h->factor_nnz = (int64_t)lval.size() + (int64_t)uval.size() + 2 * row0;
+  std::vector<int> lord = level_order(llev, &h->l_levels), uord = level_order(ulev, &h->u_levels);
+  int rc;
+  if ((rc = up(&h->layers, h->host_layers)) || (rc = up(&h->l_ptr, lptr)) || (rc = up(&h->u_ptr, uptr)) ||
+      (rc = up(&h->l_col, lcol)) || (rc = up(&h->u_col, ucol)) || (rc = up(&h->l_val, lval)) ||
+      (rc = up(&h->u_val, uval)) || (rc = up(&h->l_dinv, ldinv)) || (rc = up(&h->u_dinv, udinv)) ||
+      (rc = up(&h->l_order, lord)) || (rc = up(&h->u_order, uord)) || (rc = up(&h->q_in, qin)) ||
+      (rc = up(&h->q_out, qout)))
+    return rc;
+  LCK(cudaMalloc(&h->y, row0 * sizeof(double2)));
+  LCK(cudaMalloc(&h->w, row0 * sizeof(double2)));
+  LCK(cudaMalloc(&h->z, row0 * sizeof(double2)));
+  LCK(cudaMalloc(&h->flag, 2 * row0 * sizeof(int)));
+  LCK(cudaMemset(h->flag, 0, 2 * row0 * sizeof(int)));
+  LCK(cudaMalloc(&h->head, 2 * sizeof(int)));
+  int nsm = 0, occ = 0;
+  LCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv, 1024, 0));
+  h->grid = nsm * std::max(occ, 1);  // every warp resident: spinning warps never block a producer
+  cudaSetDevice(prev);
+  *out = h.release();
+  return 0;
+}
+
+int pt_local_destroy(pt_local* h) {
+  if (!h) return 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  delete h;
+  cudaSetDevice(prev);
+  return 0;
+}
+
+int pt_local_info(const pt_local* h, int64_t* rows, int64_t* factor_nnz, int32_t* l_levels,
+                  int32_t* u_levels) {
+  if (!h) return lfail(PT_EINVAL, "null handle");
+  if (rows) *rows = h->rows;
+  if (factor_nnz) *factor_nnz = h->factor_nnz;
+  if (l_levels) *l_levels = h->l_levels;
+  if (u_levels) *u_levels = h->u_levels;
+  return 0;
+}
+
+int pt_local_solve(pt_local* h, const double* b, double* x, pt_stream stream) {
+  if (!h || !b || !x) return lfail(PT_EINVAL, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  count_launch();
+  k_gather<<<elem_grid(h->rows), 256, 0, s>>>(h->q_in, h->layers, h->n_layers, h->rows,
+                                              (const double2*)b, h->y);
+  int rc = solve_all(h, s);
+  if (!rc) {
+    count_launch();
+    k_gather<<<elem_grid(h->rows), 256, 0, s>>>(h->q_out, h->layers, h->n_layers, h->rows, h->z,
+                                                (double2*)x);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaSetDevice(prev);
+  if (rc) return rc;
+  if (e != cudaSuccess) return lfail(PT_ECUDA, cudaGetErrorString(e));
+  return 0;
+}
+
+int pt_local_newton(pt_local* h, const double* f, double* traces, double* rhs, int32_t jump,
+                    pt_stream stream) {
+  if (!h || !f || (!traces && !rhs)) return lfail(PT_EINVAL, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  count_launch();
+  k_gather_rhs<<<elem_grid(h->rows), 256, 0, s>>>(h->layers, h->n_layers, h->q_in, h->rows,
+                                                  (const double2*)f, nullptr, 0, 0.0, h->y);
+  int rc = solve_all(h, s);
+  double2* nw = (double2*)traces;
+  if (!rc && !nw) {
+    if (!h->newton) {
+      if (cudaMalloc(&h->newton, (size_t)h->n_layers * 4 * h->nxe * sizeof(double2)) != cudaSuccess)
+        rc = lfail(PT_ECUDA, "allocation of the Newton traces failed");
+    }
+    nw = h->newton;
+  }
+  if (!rc) {
+    count_launch();
+    k_newton_out<<<dim3((unsigned)((h->nxe + 127) / 128), h->n_layers, 4), 128, 0, s>>>(
+        h->layers, h->n_layers, h->q_out, h->z, nw);
+    if (rhs) {
+      const int64_t nt_m = (int64_t)(2 * h->n_layers - 2) * h->nxe;
+      count_launch();
+      k_polarized_rhs<<<elem_grid(2 * nt_m), 256, 0, s>>>(nw, h->n_layers, (int)h->nxe, nt_m,
+                                                          jump ? 1 : 0, (double2*)rhs);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaSetDevice(prev);
+  if (rc) return rc;
+  if (e != cudaSuccess) return lfail(PT_ECUDA, cudaGetErrorString(e));
+  return 0;
+}
+
+int pt_local_reconstruct(pt_local* h, const double* f, const double* x, double hstep, double* u,
+                         pt_stream stream) {
+  if (!h || !f || !x || !u || !(hstep > 0.0)) return lfail(PT_EINVAL, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  const int64_t nt_m = (int64_t)(2 * h->n_layers - 2) * h->nxe;
+  count_launch();
+  k_gather_rhs<<<elem_grid(h->rows), 256, 0, s>>>(h->layers, h->n_layers, h->q_in, h->rows,
+                                                  (const double2*)f, (const double2*)x, nt_m,
+                                                  1.0 / (hstep * hstep), h->y);
+  int rc = solve_all(h, s);
+  if (!rc) {
+    count_launch();
+    k_volume_out<<<dim3(64, h->n_layers), 256, 0, s>>>(h->layers, h->n_layers, h->q_out, h->z,
+                                                       (double2*)u);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaSetDevice(prev);
+  if (rc) return rc;
+  if (e != cudaSuccess) return lfail(PT_ECUDA, cudaGetErrorString(e));
+  return 0;
+}
+
+}  // extern "C"

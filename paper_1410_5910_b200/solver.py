@@ -150,6 +150,8 @@ class OfflineState:
     host_state: object = None
     meta: dict = field(default_factory=dict)
     stage_seconds: dict = field(default_factory=dict)
+    # device layer factorizations (Newton traces / reconstruction on the GPU)
+    local: object = None
 
     @property
     def pol(self):
@@ -179,11 +181,19 @@ class OfflineState:
         return DevicePreconditioner(self.op, config or PreconditionerConfig())
 
     @classmethod
-    def from_case(cls, path, device=None):
+    def from_case(cls, path, device=None, local=False):
+        """A PTC1 operator cache; ``local=True`` also factors the case's layers
+        for the device Newton / reconstruction stages (offline/local.py)."""
         meta, arr = load_case_arrays(path)
         op = DeviceOperator.from_arrays(meta, arr, device=device)
         op.meta = meta
-        return cls(op=op, variant=meta.get("variant", "jump"), meta=meta)
+        state = cls(op=op, variant=meta.get("variant", "jump"), meta=meta)
+        if local:
+            from .local import DeviceLocalSolver
+            t0 = time.perf_counter()
+            state.local = DeviceLocalSolver.from_config(meta["name"], device=device)
+            state.stage_seconds["local_factor"] = time.perf_counter() - t0
+        return state
 
 
 def offline_assemble(grid, model, part, omega, *, variant="jump", factor_method="banded",
@@ -385,19 +395,52 @@ def solve_online(state: OfflineState, rhs, precond: PreconditionerConfig | None 
     return x, report
 
 
+def _solve_helmholtz_device(state, f, precond, gmres, report, oracle):
+    """Every online stage on the device: restrict + newton + rhs
+    (pt_local_newton), gmres (pt_gmres), reconstruct (pt_local_reconstruct).
+    The host copies f in and u out; one synchronisation per stage."""
+    import torch
+    loc = state.local
+
+    def stage(name, fn):
+        t0 = time.perf_counter()
+        try:
+            out = fn()
+            torch.cuda.synchronize(loc.device)
+        except Exception as exc:
+            raise RuntimeError(f"stage {name!r} failed: {exc}") from exc
+        report.stage_seconds[name] = time.perf_counter() - t0
+        return out
+
+    f_dev = stage("restrict", lambda: loc._dev(f, (loc.nz_ext, loc.nxe), "f")[0])
+    rhs = stage("rhs", lambda: loc.rhs(f_dev, state.variant))
+    x, inner = stage("gmres", lambda: solve_online(state, rhs, precond, gmres))
+    for k in ("iterations", "residual_history", "converged", "flag", "true_residual"):
+        setattr(report, k, getattr(inner, k))
+    report.traces = inner.traces
+    x_dev = x if hasattr(x, "data_ptr") else torch.from_numpy(np.asarray(x)).to(f_dev.device)
+    u = stage("reconstruct", lambda: loc.reconstruct(f_dev, x_dev))
+    report.u = u.cpu().numpy()
+    n_c = loc.geo["n_c"]
+    report.layer_fields = [report.u[n_c[i]:n_c[i + 1]] for i in range(len(n_c) - 1)]
+    if oracle is not None:
+        scale = np.linalg.norm(oracle)
+        err = np.linalg.norm(report.u - oracle)
+        report.oracle_rel_error = float(err / scale) if scale > 0 else float(err)
+    return report
+
+
 def solve_helmholtz(model, grid, part, f, *, omega=None, state: OfflineState | None = None,
                     precond=None, gmres=None, factor_method="banded", compression=None,
                     oracle=None) -> SolveReport:
     """solve_helmholtz (solver.py:308-435) with the GMRES stage on the device.
 
+    With ``state.local`` (``OfflineState.from_case(..., local=True)``) every
+    online stage runs on the device and model/grid/part are not needed; else
     restrict / newton / rhs / reconstruct are the reference's host stages
     (they need ``state.host_state``, i.e. an OfflineState from
     :func:`offline_assemble`).
     """
-    from helmsweep.local_solver import newton_trace, reconstruct_volume
-    from helmsweep.partition import restrict_source
-    from helmsweep.trace_system import TraceVector, polarized_rhs
-
     precond = precond or PreconditionerConfig()
     gmres = gmres or GmresConfig()
     report = SolveReport()
@@ -414,10 +457,16 @@ def solve_helmholtz(model, grid, part, f, *, omega=None, state: OfflineState | N
     elif state.variant != precond.variant:
         raise ValueError(f"offline state was assembled for variant {state.variant!r}, "
                          f"preconditioner wants {precond.variant!r}")
+    if state.local is not None:
+        return _solve_helmholtz_device(state, f, precond, gmres, report, oracle)
     host = state.host_state
     if host is None:
-        raise ValueError("solve_helmholtz needs the host factorizations "
-                         "(an OfflineState built by offline_assemble)")
+        raise ValueError("solve_helmholtz needs layer factorizations: an OfflineState built by "
+                         "offline_assemble, or OfflineState.from_case(..., local=True)")
+
+    from helmsweep.local_solver import newton_trace, reconstruct_volume
+    from helmsweep.partition import restrict_source
+    from helmsweep.trace_system import TraceVector, polarized_rhs
 
     def stage(name, fn):
         t0 = time.perf_counter()

@@ -1,0 +1,68 @@
+"""Host side of the device local solves, no GPU.
+
+The nested-dissection factorization of every layer (offline/local.py) must
+solve the reference's layer systems: the composed gathers q_in / q_out and the
+triangular factors, applied on the host exactly as the device applies them,
+reproduce the Newton traces behind the reference's polarized right-hand side
+(tests/golden fixtures) and the reference's volume field.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import FIXTURES, golden_path
+from paper_1410_5910_b200.cache import read_case
+from paper_1410_5910_b200.offline import configs
+from paper_1410_5910_b200.offline.assemble import polarized_rhs
+from paper_1410_5910_b200.offline.layers import edge_extend, equal_partition, layer_operator
+from paper_1410_5910_b200.offline.local import apply_factors, build_local, factor_layer, nd_order
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def test_nd_order_is_a_permutation():
+    for nze, nxe in ((7, 9), (30, 50), (1, 5), (16, 16), (40, 3)):
+        p = nd_order(nze, nxe)
+        assert np.array_equal(np.sort(p), np.arange(nze * nxe))
+
+
+def _layer_fields(name, facs, geo, f):
+    """Newton traces and polarized rhs (jump/extrapolation) on the host."""
+    newtons = []
+    nxe, n_pml = geo["nxe"], geo["n_pml"]
+    for ell, fac in enumerate(facs, start=1):
+        n = fac["n_layer"]
+        lo = n_pml + geo["n_c"][ell - 1]
+        fl = np.zeros((fac["nze"], nxe), dtype=np.complex128)
+        fl[n_pml:n_pml + n] = f[lo:lo + n]
+        w = apply_factors(fac, fl.ravel()).reshape(fac["nze"], nxe)
+        newtons.append({k: w[n_pml + k - 1] for k in (0, 1, n, n + 1)})
+    return newtons
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_host_restatement_matches_reference_rhs(name):
+    meta, arr = read_case(golden_path(name))
+    facs, geo = build_local(name, workers=1)
+    cfg = configs.config(name)
+    newtons = _layer_fields(name, facs, geo, cfg.sources[0][1])
+    rhs = polarized_rhs(newtons, geo["n_c"], meta.get("variant", "jump"))
+    assert rel(rhs, arr["rhs"][0]) <= 1e-10
+
+
+def test_factor_layer_residual_and_levels():
+    cfg = configs.config("fx_plr")
+    g = cfg.geo
+    n_c = equal_partition(g.nz, cfg.L)
+    m_ext = edge_extend(1.0 / cfg.c**2, g.n_pml)
+    lo = g.n_pml + n_c[1]
+    n_layer = int(n_c[2] - n_c[1])
+    op = layer_operator(g.nx, n_layer, g.h, g.n_pml, float(cfg.omega),
+                        edge_extend(m_ext[lo:lo + n_layer], g.n_pml, axis=0))
+    fac = factor_layer(op, n_layer + 2 * g.n_pml, g.nx_ext)
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal(op.shape[0]) + 1j * rng.standard_normal(op.shape[0])
+    assert np.linalg.norm(op @ apply_factors(fac, b) - b) <= 1e-12 * np.linalg.norm(b)
+    assert np.allclose(fac["L"].diagonal(), 1.0)
