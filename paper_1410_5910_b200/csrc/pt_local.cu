@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -64,7 +65,7 @@ struct LayerDev {
 __global__ void __launch_bounds__(1024)
 k_trsv(const int* __restrict__ order, int n, const int64_t* __restrict__ ptr,
        const int* __restrict__ col, const double2* __restrict__ val, const double2* __restrict__ dinv,
-       const double2* b, double2* x, int* flag, int epoch, int* head) {
+       const double2* b, double2* x, int* flag, int epoch, int* head, int spin_ns) {
   const int lane = threadIdx.x & 31;
   for (;;) {
     int q = 0;
@@ -76,8 +77,8 @@ k_trsv(const int* __restrict__ order, int n, const int64_t* __restrict__ ptr,
     double2 acc = make_double2(0.0, 0.0);
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const int j = __ldg(col + e);
-      while (ld_acquire(flag + j) != epoch) {
-      }
+      while (ld_acquire(flag + j) != epoch)
+        if (spin_ns) __nanosleep(spin_ns);
       acc = cfma(__ldg(val + e), ld_cg(x + j), acc);
     }
     acc = warp_sum(acc);
@@ -209,6 +210,7 @@ struct pt_local {
   int* head = nullptr;  // queue heads (2 per solve)
   int epoch = 0;
   int grid = 0;
+  int spin_ns = 0;  // back-off of a warp waiting on a dependency (PT_TRSV_SPIN)
   int64_t factor_nnz = 0;
   int32_t l_levels = 0, u_levels = 0;
   ~pt_local() {
@@ -297,7 +299,8 @@ int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) 
   k_trsv<<<h->grid, 1024, 0, s>>>(lower ? h->l_order : h->u_order, (int)h->rows,
                                   lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col,
                                   lower ? h->l_val : h->u_val, lower ? h->l_dinv : h->u_dinv, b, x,
-                                  h->flag + (lower ? 0 : h->rows), e, h->head + (lower ? 0 : 1));
+                                  h->flag + (lower ? 0 : h->rows), e, h->head + (lower ? 0 : 1),
+                                  h->spin_ns);
   LCK(cudaGetLastError());
   return 0;
 }
@@ -389,7 +392,10 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   int nsm = 0, occ = 0;
   LCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv, 1024, 0));
-  h->grid = nsm * std::max(occ, 1);  // every warp resident: spinning warps never block a producer
+  int per_sm = std::max(occ, 1);
+  if (const char* e = std::getenv("PT_TRSV_BLOCKS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+  if (const char* e = std::getenv("PT_TRSV_SPIN")) h->spin_ns = std::max(0, std::atoi(e));
+  h->grid = nsm * per_sm;  // every warp resident: spinning warps never block a producer
   cudaSetDevice(prev);
   *out = h.release();
   return 0;
