@@ -35,6 +35,12 @@ namespace pt {
 namespace {
 
 constexpr int CONSUMERS = EXEC_CONSUMERS;  // 512 threads, 16 warps
+#ifndef PT_YPLR_ILP
+#define PT_YPLR_ILP 1  // Y_PLR: two columns per iteration (c3 GMRES 19.45 -> 19.05 ms)
+#endif
+#ifndef PT_TPLR_ILP
+#define PT_TPLR_ILP 0
+#endif
 constexpr int CWARPS = CONSUMERS / 32;
 
 __shared__ double2* s_slot[N_SLOTS];
@@ -509,7 +515,18 @@ __device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, c
         it = items[r];
         const double2* V = buf + it.poff;
         const double2* x = sl.vec + it.lo;
+#if PT_TPLR_ILP
+        double2 acc2 = make_double2(0.0, 0.0);
+        int c = sub;
+        for (; c + lanes < it.n; c += 2 * lanes) {
+          acc = cfma(V[c], x[c], acc);
+          acc2 = cfma(V[c + lanes], x[c + lanes], acc2);
+        }
+        if (c < it.n) acc = cfma(V[c], x[c], acc);
+        acc = cadd(acc, acc2);
+#else
         for (int c = sub; c < it.n; c += lanes) acc = cfma(V[c], x[c], acc);
+#endif
       }
       for (int o = lanes >> 1; o > 0; o >>= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -543,17 +560,37 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
   const int r = threadIdx.x % PLR_TILE, g = threadIdx.x / PLR_TILE;
   const DevItem* items = sl.items();
   double2 acc = make_double2(0.0, 0.0);
+  double2 acc2 = make_double2(0.0, 0.0);
   for (int p = 0; p < t.npiece; ++p) {
     const DevPiece& pc = sl.pieces()[p];
     const double2* buf = wait_piece(a, L, rg, q, p);
+#if PT_YPLR_ILP
+    // two columns per iteration into two accumulators (independent loads
+    // and FMA chains), added at the end of the task in a fixed order
+    int f = pc.f0 + ((g - pc.f0) % G + G) % G;
+    for (; f + G < pc.f1; f += 2 * G) {
+      const DevItem i0 = items[f], i1 = items[f + G];
+      const double2 t0 = sl.vec[f], t1 = sl.vec[f + G];
+      const bool v0 = r >= i0.lo && r < i0.hi, v1 = r >= i1.lo && r < i1.hi;
+      const double2 u0 = v0 ? buf[i0.poff + (r - i0.lo)] : make_double2(0.0, 0.0);
+      const double2 u1 = v1 ? buf[i1.poff + (r - i1.lo)] : make_double2(0.0, 0.0);
+      acc = cfma(u0, t0, acc);
+      acc2 = cfma(u1, t1, acc2);
+    }
+    if (f < pc.f1) {
+      const DevItem it = items[f];
+      if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
+    }
+#else
     for (int f = pc.f0 + ((g - pc.f0) % G + G) % G; f < pc.f1; f += G) {
       const DevItem it = items[f];
       if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
     }
+#endif
     release_piece(L, rg);
   }
   double2* part = L.part();
-  part[g * PLR_TILE + r] = acc;
+  part[g * PLR_TILE + r] = cadd(acc, acc2);
   consumer_sync();
   if ((int)threadIdx.x < t.r1 - t.r0) {
     double2 v = epilogue_row(t, sl, threadIdx.x);
