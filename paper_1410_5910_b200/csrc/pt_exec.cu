@@ -38,6 +38,9 @@ constexpr int CONSUMERS = EXEC_CONSUMERS;  // 512 threads, 16 warps
 #ifndef PT_YPLR_ILP
 #define PT_YPLR_ILP 1  // Y_PLR: two columns per iteration (c3 GMRES 19.45 -> 19.05 ms)
 #endif
+#ifndef PT_YPLR_UNROLL
+#define PT_YPLR_UNROLL 2
+#endif
 #ifndef PT_TPLR_ILP
 #define PT_TPLR_ILP 0
 #endif
@@ -565,19 +568,31 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
     const DevPiece& pc = sl.pieces()[p];
     const double2* buf = wait_piece(a, L, rg, q, p);
 #if PT_YPLR_ILP
-    // two columns per iteration into two accumulators (independent loads
-    // and FMA chains), added at the end of the task in a fixed order
+    // PT_YPLR_UNROLL columns per iteration, alternately into two accumulators
+    // (independent loads and FMA chains), added at the end in a fixed order
     int f = pc.f0 + ((g - pc.f0) % G + G) % G;
-    for (; f + G < pc.f1; f += 2 * G) {
-      const DevItem i0 = items[f], i1 = items[f + G];
-      const double2 t0 = sl.vec[f], t1 = sl.vec[f + G];
-      const bool v0 = r >= i0.lo && r < i0.hi, v1 = r >= i1.lo && r < i1.hi;
-      const double2 u0 = v0 ? buf[i0.poff + (r - i0.lo)] : make_double2(0.0, 0.0);
-      const double2 u1 = v1 ? buf[i1.poff + (r - i1.lo)] : make_double2(0.0, 0.0);
-      acc = cfma(u0, t0, acc);
-      acc2 = cfma(u1, t1, acc2);
+    for (; f + (PT_YPLR_UNROLL - 1) * G < pc.f1; f += PT_YPLR_UNROLL * G) {
+      DevItem it[PT_YPLR_UNROLL];
+      double2 tv[PT_YPLR_UNROLL], uv[PT_YPLR_UNROLL];
+#pragma unroll
+      for (int u = 0; u < PT_YPLR_UNROLL; ++u) {
+        it[u] = items[f + u * G];
+        tv[u] = sl.vec[f + u * G];
+      }
+#pragma unroll
+      for (int u = 0; u < PT_YPLR_UNROLL; ++u) {
+        const bool v = r >= it[u].lo && r < it[u].hi;
+        uv[u] = v ? buf[it[u].poff + (r - it[u].lo)] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < PT_YPLR_UNROLL; ++u) {
+        if (u & 1)
+          acc2 = cfma(uv[u], tv[u], acc2);
+        else
+          acc = cfma(uv[u], tv[u], acc);
+      }
     }
-    if (f < pc.f1) {
+    for (; f < pc.f1; f += G) {
       const DevItem it = items[f];
       if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
     }
