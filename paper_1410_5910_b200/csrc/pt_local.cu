@@ -74,17 +74,23 @@ k_trsv(const int* __restrict__ order, int n, const int64_t* __restrict__ ptr,
     if (q >= n) return;
     const int i = __ldg(order + q);
     const int64_t e0 = __ldg(ptr + i), e1 = __ldg(ptr + i + 1);
+    // the row's own data (factor entries, rhs, 1/diagonal) is loaded before
+    // any dependency wait, so only the x loads follow a satisfied flag
+    // (a warp-per-separator variant that kept dense separator runs in shared
+    // memory serialised these loads and measured 2.2x slower)
+    const double2 bi = lane == 0 ? ld_cg(b + i) : make_double2(0.0, 0.0);
+    const double2 di = lane == 0 ? __ldg(dinv + i) : make_double2(0.0, 0.0);
     double2 acc = make_double2(0.0, 0.0);
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const int j = __ldg(col + e);
+      const double2 v = __ldg(val + e);
       while (ld_acquire(flag + j) != epoch)
         if (spin_ns) __nanosleep(spin_ns);
-      acc = cfma(__ldg(val + e), ld_cg(x + j), acc);
+      acc = cfma(v, ld_cg(x + j), acc);
     }
     acc = warp_sum(acc);
     if (lane == 0) {
-      const double2 r = csub(ld_cg(b + i), acc);
-      st_cg(x + i, cmul(r, __ldg(dinv + i)));
+      st_cg(x + i, cmul(csub(bi, acc), di));
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag + i), "r"(epoch) : "memory");
     }
   }
@@ -392,8 +398,8 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   int nsm = 0, occ = 0;
   LCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv, 1024, 0));
-  int per_sm = std::max(occ, 1);
-  if (const char* e = std::getenv("PT_TRSV_BLOCKS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+  int per_sm = 1;  // one block of 32 warps per SM (measured faster than two at c3)
+  if (const char* e = std::getenv("PT_TRSV_BLOCKS")) per_sm = std::max(1, std::min(std::max(occ, 1), std::atoi(e)));
   if (const char* e = std::getenv("PT_TRSV_SPIN")) h->spin_ns = std::max(0, std::atoi(e));
   h->grid = nsm * per_sm;  // every warp resident: spinning warps never block a producer
   cudaSetDevice(prev);
