@@ -170,6 +170,7 @@ struct pt_handle {
     PlanParams pp;
     int grid = 0;  // persistent CTAs of the batched executor
     int rows = BT_ROWS;  // output rows per task (8 or 16)
+    int tcols = BW;      // sources per task (64, or 32: every task split in two)
     double2* slot[N_SLOTS] = {nullptr};
     int64_t slot_cap[N_SLOTS] = {0};
     int* ctr = nullptr;
@@ -1223,7 +1224,9 @@ int batch_init(pt_handle* h) {
   CK(bexec_setup());
   CK(bg_setup(1));
   if (const char* e = std::getenv("PT_BATCH_ROWS")) B.rows = std::atoi(e) == 16 ? 16 : 8;
-  B.grid = bexec_grid(h->device, B.rows);
+  if (const char* e = std::getenv("PT_BATCH_COLS")) B.tcols = std::atoi(e) == 32 ? 32 : BW;
+  if (B.tcols == 32) B.rows = 16;  // the 16 x 32 tile
+  B.grid = bexec_grid(h->device, B.rows, B.tcols);
   if (B.grid <= 0) return fail(PT_ECUDA, "batched executor does not fit on an SM");
   B.pp = h->pp;
   B.pp.ctas = B.grid;
@@ -1280,6 +1283,21 @@ int get_bprogram(pt_handle* h, const std::string& kind, int n_it, DevProgram** o
   for (const DevTask& t : p->host.tasks)
     if (t.type != TASK_Y_DENSE || t.nterm > BT_TERMS || t.neye > BT_EYES || t.r1 - t.r0 > B.rows)
       return fail(PT_EINVAL, "a task exceeds what the batched executor stages");
+  if (B.tcols < BW) {
+    // every task becomes BW / tcols tasks over disjoint source columns (same
+    // waits; each producer group counts all of them)
+    const int split = BW / B.tcols;
+    std::vector<DevTask> tasks;
+    for (const DevTask& t : p->host.tasks)
+      for (int c = 0; c < split; ++c) {
+        DevTask u = t;
+        u.c0 = c * B.tcols;
+        u.c1 = u.c0 + B.tcols;
+        tasks.push_back(u);
+      }
+    p->host.tasks.swap(tasks);
+    for (DevWait& w : p->host.waits) w.val *= split;
+  }
   if ((rc = upload(&p->tasks, p->host.tasks))) return rc;
   if ((rc = upload(&p->terms, p->host.terms))) return rc;
   if ((rc = upload(&p->eyes, p->host.eyes))) return rc;
@@ -1333,7 +1351,7 @@ int run_bprogram(pt_handle* h, DevProgram* p, const double2* in, double2* out, c
     }
     CK(cudaEventRecord(e0, s));
   }
-  CK(bexec_launch(a, B.grid, B.rows, s));
+  CK(bexec_launch(a, B.grid, B.rows, B.tcols, s));
   if (h->timing) {
     CK(cudaEventRecord(e1, s));
     h->ev_used.emplace_back(e0, e1);

@@ -29,13 +29,13 @@ extern void count_launch();
 namespace {
 
 constexpr int AS_LD = BT_KC + 4;  // A rows 4 apart mod 8 (16-byte units): conflict-free fragments
-constexpr int XS_LD = BW + 2;     // X rows 2 apart mod 8: conflict-free B fragments
-constexpr int XS_ELEMS = BT_KC * XS_LD;
-template <int ROWS>
+// X chunk rows: COLS + 2 complex (2 apart mod 8 in 16-byte units: conflict-free B fragments)
+template <int COLS>
+constexpr int xs_ld() { return COLS + 2; }
+template <int ROWS, int COLS>
 constexpr size_t bexec_smem() {
-  return (size_t)(2 * ROWS * AS_LD + 2 * XS_ELEMS) * sizeof(double2);
+  return (size_t)(2 * ROWS * AS_LD + 2 * BT_KC * xs_ld<COLS>()) * sizeof(double2);
 }
-static_assert(BT_KC * BW == 4 * BT_THREADS, "four X values per thread per chunk");
 static_assert(BW == 64 && BT_THREADS == 256, "warp tiling assumes 8 warps over 64 sources");
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -57,13 +57,19 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// ROWS = 16: 8 warps = 2 row groups x 4 column groups of 16 sources (two
-// n-tiles each); ROWS = 8: 1 row group x 8 column groups of 8 sources.
-template <int ROWS>
+// A task covers ROWS output rows and COLS of the 64 sources (columns
+// [c0, c0 + COLS), c0 = the task's c0 field).  ROWS x COLS = 16 x 64: 8 warps =
+// 2 row groups x 4 column groups of 16 sources (two n-tiles each); 8 x 64:
+// 1 x 8 groups of 8 sources; 16 x 32: 2 x 4 groups of 8 sources.
+template <int ROWS, int COLS>
 __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BExecArgs a) {
   constexpr int RG = ROWS / 8;           // row groups of 8
   constexpr int CG = 8 / RG;             // column groups
-  constexpr int NT = BW / CG / 8;        // n-tiles (8 sources) per warp
+  constexpr int NT = COLS / CG / 8;      // n-tiles (8 sources) per warp
+  constexpr int XU = COLS / 16;          // X values per thread per chunk (16 threads per row)
+  constexpr int XS_LD = xs_ld<COLS>();
+  constexpr int XS_ELEMS = BT_KC * XS_LD;
+  static_assert(NT >= 1 && BT_KC * COLS == XU * BT_THREADS, "tiling");
   constexpr int AS_ELEMS = ROWS * AS_LD;
   extern __shared__ __align__(16) double2 bsm[];
   double2* As = bsm;                 // [2][ROWS][AS_LD]  kernel rows of the chunk
@@ -116,6 +122,7 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
     }
     __syncthreads();
     const int r0 = s_task.r0, nrows = s_task.r1 - s_task.r0;
+    const int cb = COLS == BW ? 0 : s_task.c0;  // the task's first source column
     const int nch = nterm * kchunks;
 
     auto load_A = [&](int c, int buf) {
@@ -128,21 +135,21 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
       }
       cp_commit();
     };
-    double2 xa[4], xb[4];
+    double2 xa[XU], xb[XU];
     auto load_X = [&](int c) {
       const int term = c / kchunks, kc = (c - term * kchunks) * BT_KC;
       const DevTerm& tm = s_terms[term];
       const int64_t row = kc + kr;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xa[u] = xb[u] = make_double2(0.0, 0.0);
+      for (int u = 0; u < XU; ++u) xa[u] = xb[u] = make_double2(0.0, 0.0);
       if (row < m) {
-        const double2* p0 = s_vec[tm.src[0].slot] + (tm.src[0].off + row) * BW + xc;
+        const double2* p0 = s_vec[tm.src[0].slot] + (tm.src[0].off + row) * BW + cb + xc;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) xa[u] = ld_cg(p0 + 16 * u);
+        for (int u = 0; u < XU; ++u) xa[u] = ld_cg(p0 + 16 * u);
         if (tm.nsrc > 1) {
-          const double2* p1 = s_vec[tm.src[1].slot] + (tm.src[1].off + row) * BW + xc;
+          const double2* p1 = s_vec[tm.src[1].slot] + (tm.src[1].off + row) * BW + cb + xc;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) xb[u] = ld_cg(p1 + 16 * u);
+          for (int u = 0; u < XU; ++u) xb[u] = ld_cg(p1 + 16 * u);
         }
       }
     };
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
       const double2 sc = make_double2(tm.scale_re, tm.scale_im);
       double2* d = Xs + buf * XS_ELEMS + kr * XS_LD + xc;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d[16 * u] = cmul(sc, cadd(xa[u], xb[u]));
+      for (int u = 0; u < XU; ++u) d[16 * u] = cmul(sc, cadd(xa[u], xb[u]));
     };
     double acc[NT][2][2];  // [n-tile][re, im][pair]
 #pragma unroll
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(BT_THREADS, BT_CTAS_PER_SM) pt_bexec_kernel(BE
     // epilogue: rows wr + lane/4, columns wc + 8u + 2(lane%4) + e
     const int orow = wr + (lane >> 2);
     if (orow < nrows) {
-      const int64_t rb = (int64_t)(r0 + orow) * BW;
+      const int64_t rb = (int64_t)(r0 + orow) * BW + cb;
       double2* outp = s_vec[s_task.out.slot] + s_task.out.off * BW + rb;
       const double2* initp = s_task.has_init ? s_vec[s_task.init.slot] + s_task.init.off * BW + rb : nullptr;
       const double2* rhsp = s_task.has_rhs ? s_vec[s_task.rhs.slot] + s_task.rhs.off * BW + rb : nullptr;
@@ -663,36 +670,46 @@ int elem_grid(int64_t n) {
 
 }  // namespace
 
+#define PT_BEXEC_VARIANTS(X) X(16, 64) X(8, 64) X(16, 32)
+
 cudaError_t bexec_setup() {
-  for (const void* f : {(const void*)pt_bexec_kernel<16>, (const void*)pt_bexec_kernel<8>}) {
-    const int smem = (int)(f == (const void*)pt_bexec_kernel<16> ? bexec_smem<16>() : bexec_smem<8>());
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+  cudaError_t e = cudaSuccess;
+#define PT_SETUP(R, C)                                                                      \
+  if (e == cudaSuccess)                                                                     \
+    e = cudaFuncSetAttribute(pt_bexec_kernel<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)bexec_smem<R, C>());                                      \
+  if (e == cudaSuccess)                                                                     \
+    e = cudaFuncSetAttribute(pt_bexec_kernel<R, C>, cudaFuncAttributePreferredSharedMemoryCarveout, \
                              (int)cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  PT_BEXEC_VARIANTS(PT_SETUP)
+#undef PT_SETUP
+  return e;
 }
 
-int bexec_grid(int device, int rows) {
+int bexec_grid(int device, int rows, int cols) {
   int nsm = 0, occ = 0;
   if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  cudaError_t e = rows == 8 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_bexec_kernel<8>,
-                                                                            BT_THREADS, bexec_smem<8>())
-                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_bexec_kernel<16>,
-                                                                            BT_THREADS, bexec_smem<16>());
+  cudaError_t e = cudaErrorInvalidValue;
+#define PT_OCC(R, C)                                                                          \
+  if (rows == R && cols == C)                                                                 \
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt_bexec_kernel<R, C>, BT_THREADS, \
+                                                      bexec_smem<R, C>());
+  PT_BEXEC_VARIANTS(PT_OCC)
+#undef PT_OCC
   if (e != cudaSuccess) return 0;
   return nsm * std::max(occ, 1);
 }
 
-cudaError_t bexec_launch(const BExecArgs& a, int grid, int rows, cudaStream_t s) {
+cudaError_t bexec_launch(const BExecArgs& a, int grid, int rows, int cols, cudaStream_t s) {
   count_launch();
-  if (rows == 8)
-    pt_bexec_kernel<8><<<grid, BT_THREADS, bexec_smem<8>(), s>>>(a);
-  else
-    pt_bexec_kernel<16><<<grid, BT_THREADS, bexec_smem<16>(), s>>>(a);
-  return cudaGetLastError();
+#define PT_LAUNCH(R, C)                                                   \
+  if (rows == R && cols == C) {                                           \
+    pt_bexec_kernel<R, C><<<grid, BT_THREADS, bexec_smem<R, C>(), s>>>(a); \
+    return cudaGetLastError();                                            \
+  }
+  PT_BEXEC_VARIANTS(PT_LAUNCH)
+#undef PT_LAUNCH
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t bg_setup(int max_iter) {

@@ -62,8 +62,10 @@ struct BGmresDev {
 };
 
 // one batched program launch (persistent, grid = bexec_grid())
-cudaError_t bexec_launch(const BExecArgs& a, int grid, int rows, cudaStream_t s);
-int bexec_grid(int device, int rows);
+// tiles: rows x cols = 16 x 64, 8 x 64 or 16 x 32 (cols < 64: tasks carry
+// their first source column in DevTask::c0)
+cudaError_t bexec_launch(const BExecArgs& a, int grid, int rows, int cols, cudaStream_t s);
+int bexec_grid(int device, int rows, int cols);
 cudaError_t bexec_setup();
 
 // batched GMRES steps (graph-capturable; see pt_batch.cu)
