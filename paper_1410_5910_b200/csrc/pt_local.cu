@@ -65,14 +65,18 @@ struct LayerDev {
 __global__ void __launch_bounds__(1024)
 k_trsv(const int* __restrict__ order, int n, const int64_t* __restrict__ ptr,
        const int* __restrict__ col, const double2* __restrict__ val, const double2* __restrict__ dinv,
-       const double2* b, double2* x, int* flag, int epoch, int* head, int spin_ns) {
+       const double2* b, double2* x, int* flag, int epoch, int* head, int spin_ns, int chunk) {
   const int lane = threadIdx.x & 31;
+  int q = 0, qend = 0;
   for (;;) {
-    int q = 0;
-    if (lane == 0) q = atomicAdd(head, 1);
-    q = __shfl_sync(0xffffffffu, q, 0);
+    // `chunk` consecutive queue positions per grab (fewer same-address atomics)
+    if (q >= qend) {
+      if (lane == 0) q = atomicAdd(head, chunk);
+      q = __shfl_sync(0xffffffffu, q, 0);
+      qend = min(q + chunk, n);
+    }
     if (q >= n) return;
-    const int i = __ldg(order + q);
+    const int i = __ldg(order + q++);
     const int64_t e0 = __ldg(ptr + i), e1 = __ldg(ptr + i + 1);
     // the row's own data (factor entries, rhs, 1/diagonal) is loaded before
     // any dependency wait, so only the x loads follow a satisfied flag
@@ -217,6 +221,7 @@ struct pt_local {
   int epoch = 0;
   int grid = 0;
   int spin_ns = 0;  // back-off of a warp waiting on a dependency (PT_TRSV_SPIN)
+  int chunk = 2;    // queue positions per grab (PT_TRSV_CHUNK; 2 measured best)
   int64_t factor_nnz = 0;
   int32_t l_levels = 0, u_levels = 0;
   ~pt_local() {
@@ -306,7 +311,7 @@ int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) 
                                   lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col,
                                   lower ? h->l_val : h->u_val, lower ? h->l_dinv : h->u_dinv, b, x,
                                   h->flag + (lower ? 0 : h->rows), e, h->head + (lower ? 0 : 1),
-                                  h->spin_ns);
+                                  h->spin_ns, h->chunk);
   LCK(cudaGetLastError());
   return 0;
 }
@@ -401,6 +406,7 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   int per_sm = 1;  // one block of 32 warps per SM (measured faster than two at c3)
   if (const char* e = std::getenv("PT_TRSV_BLOCKS")) per_sm = std::max(1, std::min(std::max(occ, 1), std::atoi(e)));
   if (const char* e = std::getenv("PT_TRSV_SPIN")) h->spin_ns = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("PT_TRSV_CHUNK")) h->chunk = std::max(1, std::atoi(e));
   h->grid = nsm * per_sm;  // every warp resident: spinning warps never block a producer
   cudaSetDevice(prev);
   *out = h.release();

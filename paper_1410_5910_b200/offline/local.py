@@ -4,9 +4,11 @@ The reference factors every layer operator with SuperLU (COLAMD column order,
 ``LocalFactorization``, local_solver.py:21-60) and solves on the host.  For
 the device the same layer operator (``layers.layer_operator``) is factored
 once with a geometric nested-dissection order of its nze x nxe grid, which
-keeps the dependency depth of the triangular solves short (c3 layer: ~900
-levels against ~8,400 with COLAMD), and diagonal pivoting (the layer
-operators are diagonally dominant enough; residuals ~1e-13 are checked):
+keeps the dependency depth of the triangular solves short (c3 layer: 738
+levels and 7.9 M stored entries with 4 x 4 leaf blocks -- 903 levels and
+12.1 M with 16 x 16 leaves, 8,421 levels with SuperLU's COLAMD order), and
+diagonal pivoting (the layer operators are diagonally dominant enough;
+residuals ~1e-13 are checked):
 
     P A P^T = A',   Pr A' Pc = L U   (SuperLU, permc NATURAL on A')
 
@@ -29,7 +31,7 @@ from .layers import edge_extend, equal_partition, layer_operator
 __all__ = ["nd_order", "factor_layer", "build_local", "apply_factors"]
 
 
-def nd_order(nze, nxe, min_block=16):
+def nd_order(nze, nxe, min_block=4):
     """Geometric nested dissection of the nze x nxe grid (index z * nxe + x):
     split the longer side by a grid line, order both halves, then the line."""
     out = []
