@@ -156,3 +156,26 @@ def test_c5_batched_parity(cuda_ok):
         assert rel(X[s][: nt * m] + X[s][nt * m:], arr["ref_traces"][i]) <= TRACE_TOL
     for r in reps:
         assert r["converged"] and r["true_residual"] <= 10 * meta["gmres_tol"]
+
+
+@pytest.mark.parametrize("tile", [("PT_BATCH_ROWS", "8"), ("PT_BATCH_ROWS", "16"), ("PT_BATCH_COLS", "32")])
+def test_batch_tiles_agree(cuda_ok, tile, monkeypatch):
+    """Every batched tile shape (16x32 default, 8x64, 16x64) gives the same
+    applies to rounding and the same per-source iterations."""
+    from paper_1410_5910_b200.operator import DeviceOperator, load_case_arrays
+    from conftest import golden_path
+    meta, arr = load_case_arrays(golden_path("fx_uneven"))
+    monkeypatch.setenv(*tile)
+    op = DeviceOperator.from_arrays(meta, arr)  # fresh handle: the tile is read at first use
+    X = sources(40, op.N, 21)
+    pol, perm = O.operator_from_case(meta, arr)
+    d, r = O.split_dr(pol, perm)
+    Z = op.apply_M_batch(X)
+    for s in (0, 17, 39):
+        assert rel(Z[s], O.preconditioner_apply(2, d, r, perm, X[s])) <= APPLY_TOL
+    Xs, reps = op.gmres_batch(X[:6], rel_tol=meta["gmres_tol"])
+    for s in range(6):
+        x1, r1 = op.gmres(X[s], rel_tol=meta["gmres_tol"])
+        assert abs(reps[s]["iterations"] - r1["iterations"]) <= 1
+        assert rel(Xs[s], x1) <= TRACE_TOL
+    op.close()
