@@ -147,22 +147,24 @@ __device__ void givens_update(const GmresDev& g, int j, double rel_tol, int max_
   const int ldr = g.max_iter + 1;
   double2* Rj = g.R + (int64_t)j * ldr;
   double2* Hj = g.Hraw + (int64_t)j * ldr;
-  for (int i = 0; i <= j; ++i) {
-    const double2 h = cadd(ld_cg(g.h1 + i), ld_cg(g.h2 + i));
-    Rj[i] = h;
-    Hj[i] = h;
-  }
   const double hn = sqrt(ld_cg(g.hn2).x);
   Hj[j + 1] = make_double2(hn, 0.0);
+  // previous rotations down the new column; the running entry is carried in
+  // registers and every load (h, cs, sn) is independent of the rotation
+  // chain, so only the FMA chain is serial (a store/load round trip per
+  // rotation through memory would cost ~1 us each)
+  double2 a = cadd(ld_cg(g.h1), ld_cg(g.h2));
+  Hj[0] = a;
+#pragma unroll 4
   for (int i = 0; i < j; ++i) {
+    const double2 b = cadd(ld_cg(g.h1 + i + 1), ld_cg(g.h2 + i + 1));
+    Hj[i + 1] = b;
     const double c = g.cs[i];
     const double2 s = g.sn[i];
-    const double2 a = Rj[i], b = Rj[i + 1];
     Rj[i] = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
-    Rj[i + 1] = cadd(cmul(make_double2(-s.x, s.y), a), make_double2(c * b.x, c * b.y));
+    a = cadd(cmul(make_double2(-s.x, s.y), a), make_double2(c * b.x, c * b.y));
   }
   // rotation zeroing hn below Rj[j]:  [c s; -conj(s) c] [a; hn] = [r; 0]
-  const double2 a = Rj[j];
   const double aa = sqrt(cabs2(a));
   double c;
   double2 s, rr;
