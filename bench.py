@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, help="case name (default: c3, else c2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-online", action="store_true",
+                    help="skip the whole-online-stage line (Newton + GMRES + reconstruction)")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU sample")
     return ap.parse_args()
 
@@ -243,6 +245,41 @@ def run_reference(args):
 # ----------------------------------------------------------------------------
 
 
+def online_pipeline(name, meta, op, device, tol):
+    """The whole online stage of solve_helmholtz on the device (restrict,
+    Newton traces + polarized rhs, GMRES, reconstruction),
+    best of 3 after a warm-up, next to the reference's own host stage seconds
+    recorded with the case.  Reported beside the metric, not part of it."""
+    import torch
+    from paper_1410_5910_b200 import solver as S
+    from paper_1410_5910_b200.local import DeviceLocalSolver
+    from paper_1410_5910_b200.offline.configs import config as case_config
+    t0 = time.perf_counter()
+    loc = DeviceLocalSolver.from_config(name, device=device)
+    factor_s = time.perf_counter() - t0
+    state = S.OfflineState(op=op, variant=meta.get("variant", "jump"), meta=meta, local=loc)
+    f = case_config(name).sources[0][1]
+    cfg = S.GmresConfig(rel_tol=tol)
+    runs = []
+    for _ in range(4):
+        rep = S.solve_helmholtz(None, None, None, f, state=state, gmres=cfg)
+        runs.append(rep.stage_seconds)
+    best = {k: min(r[k] for r in runs[1:]) * 1e3 for k in runs[0]}
+    ref = (meta.get("solves") or [{}])[0].get("stage_seconds", {})
+    ref_ms = {k: v * 1e3 for k, v in ref.items()
+              if k in ("restrict", "newton", "rhs", "gmres", "reconstruct")}
+    out = {"device_stage_ms": best, "device_total_ms": sum(best.values()),
+           "iterations": rep.iterations, "local_factor_host_s": factor_s,
+           "local_levels": loc.info["l_levels"],
+           "reference_host_stage_ms": ref_ms or None,
+           "reference_host_total_ms": sum(ref_ms.values()) if ref_ms else None,
+           "note": "per-stage wall time, device synchronised per stage; reference stage "
+                   "seconds recorded with the case (8-core container)"}
+    loc.close()
+    torch.cuda.synchronize(device)
+    return out
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_setup("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else None)
@@ -373,6 +410,10 @@ def run_ours(args):
         trace_err = None
     k = rep_chk["iterations"]
 
+    online = None
+    if world == 1 and not batched and not args.no_online:
+        online = online_pipeline(name, meta, op, local, tol)
+
     if rank != 0:
         return
     peak, peak_src = peaks()
@@ -432,6 +473,8 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if online is not None:
+        line["online_pipeline"] = online
     if world == 1 and not args.no_cpu_baseline:
         est, s, t = cpu_sample(meta, arr, args.cpu_budget, k)
         line["cpu_baseline"] = {

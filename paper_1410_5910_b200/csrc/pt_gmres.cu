@@ -59,25 +59,6 @@ __device__ void block_sum_chunk(double2 (&acc)[RED_CHUNK], double2 (*red)[RED_CH
   __syncthreads();
 }
 
-// P[b, i] = sum_{e in block b} conj(V_i[e]) w[e]
-__device__ void dots_pass(const double2* V, int64_t ldv, int ncols, const double2* w,
-                          int64_t lo, int64_t hi, double2* Prow) {
-  __shared__ double2 red[RED_THREADS / 32][RED_CHUNK];
-  for (int c0 = 0; c0 < ncols; c0 += RED_CHUNK) {
-    double2 acc[RED_CHUNK];
-#pragma unroll
-    for (int u = 0; u < RED_CHUNK; ++u) acc[u] = make_double2(0.0, 0.0);
-    const int cnt = ncols - c0 < RED_CHUNK ? ncols - c0 : RED_CHUNK;
-    for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
-      const double2 wv = ld_cg(w + e);
-#pragma unroll
-      for (int u = 0; u < RED_CHUNK; ++u)
-        if (u < cnt) acc[u] = cfma_conj(ld_cg(V + (int64_t)(c0 + u) * ldv + e), wv, acc[u]);
-    }
-    block_sum_chunk(acc, red, Prow + c0, cnt);
-  }
-}
-
 __device__ void norm_pass(const double2* w, int64_t lo, int64_t hi, double2* outp) {
   __shared__ double2 red[RED_THREADS / 32][RED_CHUNK];
   double2 acc[RED_CHUNK];
@@ -89,16 +70,6 @@ __device__ void norm_pass(const double2* w, int64_t lo, int64_t hi, double2* out
     acc[0].x = fma(v.y, v.y, acc[0].x);
   }
   block_sum_chunk(acc, red, outp, 1);
-}
-
-// w -= V hs, in place; own elements only
-__device__ void update_pass(const double2* V, int64_t ldv, int ncols, const double2* hs,
-                            double2* w, int64_t lo, int64_t hi) {
-  for (int64_t e = lo + threadIdx.x; e < hi; e += RED_THREADS) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int i = 0; i < ncols; ++i) acc = cfma(ld_cg(V + (int64_t)i * ldv + e), hs[i], acc);
-    st_cg(w + e, csub(ld_cg(w + e), acc));
-  }
 }
 
 // The last block to arrive sums the partials of all blocks (index order).
