@@ -255,6 +255,13 @@ typedef struct {
   const int32_t *u_col;
   const double *u_val;
   const int64_t *q_in, *q_out; /* dim each, layer-local indices */
+  /* optional: the factor order's nested-dissection blocks (leaf blocks and
+   * separators, contiguous rows): block k is rows [block_ptr[k],
+   * block_ptr[k+1]).  With them every block is solved in two parallel steps
+   * through the inverse of its diagonal block (formed at create); without
+   * (n_blocks = 0), one row at a time. */
+  int64_t n_blocks;
+  const int64_t *block_ptr;    /* n_blocks + 1 */
 } pt_local_layer;
 /* layers in depth order (layer l's interior rows follow layer l-1's) */
 int pt_local_create(const pt_local_layer *layers, int32_t n_layers, int device,

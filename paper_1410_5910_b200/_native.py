@@ -53,7 +53,8 @@ class LocalLayer(C.Structure):
                 ("n_layer", C.c_int64), ("n_pml", C.c_int64),
                 ("l_ptr", C.c_void_p), ("l_col", C.c_void_p), ("l_val", C.c_void_p),
                 ("u_ptr", C.c_void_p), ("u_col", C.c_void_p), ("u_val", C.c_void_p),
-                ("q_in", C.c_void_p), ("q_out", C.c_void_p)]
+                ("q_in", C.c_void_p), ("q_out", C.c_void_p),
+                ("n_blocks", C.c_int64), ("block_ptr", C.c_void_p)]
 
 
 _VP = C.c_void_p

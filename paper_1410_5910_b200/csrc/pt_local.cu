@@ -100,6 +100,64 @@ k_trsv(const int* __restrict__ order, int n, const int64_t* __restrict__ ptr,
   }
 }
 
+// ---- block triangular solve (one CTA per nested-dissection block) ----------
+// The factor order is the nested-dissection order, so every leaf block and
+// separator is a contiguous run of rows whose diagonal block L_SS (U_SS) is
+// triangular and dense enough to invert once at create time.  A block's solve
+// is then two parallel steps: r = b_S - L_S,ext x_ext (the entries outside the
+// block, behind the global flags of earlier blocks), x_S = L_SS^-1 r (a dense
+// product) -- instead of one flag round trip per row of the block.  Blocks are
+// queued by their dependency level (the depth of the dissection tree).
+constexpr int TRSV_BLOCK_MAX = 256;
+constexpr int TRSV_BLOCK_THREADS = 256;
+__global__ void __launch_bounds__(TRSV_BLOCK_THREADS)
+k_trsv_block(const int* __restrict__ border, const int* __restrict__ bstart,
+             const int* __restrict__ blen, const int64_t* __restrict__ boff,
+             const double2* __restrict__ binv, int nblocks, const int64_t* __restrict__ ptr,
+             const int* __restrict__ col, const double2* __restrict__ val, const double2* b,
+             double2* x, int* flag, int epoch, int* head, int spin_ns) {
+  __shared__ double2 r[TRSV_BLOCK_MAX];
+  __shared__ int s_q;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) s_q = atomicAdd(head, 1);
+    __syncthreads();
+    const int q = s_q;
+    if (q >= nblocks) return;
+    const int blk = __ldg(border + q);
+    const int s0 = __ldg(bstart + blk), len = __ldg(blen + blk);
+    // r = b_S - (entries outside the block) . x
+    for (int k = wid; k < len; k += nw) {
+      const int i = s0 + k;
+      const int64_t e0 = __ldg(ptr + i), e1 = __ldg(ptr + i + 1);
+      double2 acc = make_double2(0.0, 0.0);
+      for (int64_t e = e0 + lane; e < e1; e += 32) {
+        const int j = __ldg(col + e);
+        if (j >= s0 && j < s0 + len) continue;  // inside the block: the inverse handles it
+        const double2 v = __ldg(val + e);
+        while (ld_acquire(flag + j) != epoch)
+          if (spin_ns) __nanosleep(spin_ns);
+        acc = cfma(v, ld_cg(x + j), acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) r[k] = csub(ld_cg(b + i), acc);
+    }
+    __syncthreads();
+    // x_S = inv(L_SS) r (row k of the inverse is contiguous)
+    const double2* inv = binv + __ldg(boff + blk);
+    for (int k = wid; k < len; k += nw) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int j = lane; j < len; j += 32) acc = cfma(__ldg(inv + (int64_t)k * len + j), r[j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        st_cg(x + s0 + k, acc);
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag + s0 + k), "r"(epoch) : "memory");
+      }
+    }
+    __syncthreads();  // r is reused by the next block
+  }
+}
+
 // y[G] = b_layer[q_in[k]] for every global row G = row0 + k.  b_layer is the
 // layer's forcing in natural (z, x) order: f restricted to the layer rows
 // (restrict_source, partition.py:104-113) plus, when x_traces is given, the
@@ -224,11 +282,20 @@ struct pt_local {
   int chunk = 2;    // queue positions per grab (PT_TRSV_CHUNK; 2 measured best)
   int64_t factor_nnz = 0;
   int32_t l_levels = 0, u_levels = 0;
+  // block solve (k_trsv_block): blocks, their inverses, queues by level
+  bool blocked = false;  // every layer passed its dissection blocks (PT_TRSV_BLOCK=0: off)
+  int nblocks = 0;
+  int *bstart = nullptr, *blen = nullptr, *l_border = nullptr, *u_border = nullptr;
+  int64_t *l_boff = nullptr, *u_boff = nullptr;
+  double2 *l_binv = nullptr, *u_binv = nullptr;
+  int bgrid = 0;
+  int32_t l_blevels = 0, u_blevels = 0;
   ~pt_local() {
     for (void* p : {(void*)layers, (void*)l_ptr, (void*)u_ptr, (void*)l_col, (void*)u_col,
                     (void*)l_val, (void*)u_val, (void*)l_dinv, (void*)u_dinv, (void*)l_order,
                     (void*)u_order, (void*)q_in, (void*)q_out, (void*)y, (void*)w, (void*)z, (void*)newton,
-                    (void*)flag, (void*)head})
+                    (void*)flag, (void*)head, (void*)bstart, (void*)blen, (void*)l_border,
+                    (void*)u_border, (void*)l_boff, (void*)u_boff, (void*)l_binv, (void*)u_binv})
       cudaFree(p);
   }
 };
@@ -304,9 +371,82 @@ std::vector<int> level_order(const std::vector<int>& level, int32_t* nlev) {
   return order;
 }
 
+// Inverse of the dense diagonal block rows/cols [s0, s0 + n) of one factor
+// (off-diagonal CSR with global columns + 1/diagonal), row-major, appended
+// to inv.  Lower: forward substitution per column; upper: backward.
+void invert_block(const std::vector<int64_t>& ptr, const std::vector<int>& col,
+                  const std::vector<double2>& val, const std::vector<double2>& dinv, int64_t s0,
+                  int n, bool lower, std::vector<double2>& inv) {
+  std::vector<double2> D((size_t)n * n, make_double2(0.0, 0.0));  // strict part
+  for (int k = 0; k < n; ++k)
+    for (int64_t e = ptr[s0 + k]; e < ptr[s0 + k + 1]; ++e) {
+      const int64_t j = col[e] - s0;
+      if (j >= 0 && j < n) D[(size_t)k * n + j] = val[e];
+    }
+  const size_t base = inv.size();
+  inv.resize(base + (size_t)n * n, make_double2(0.0, 0.0));
+  double2* X = inv.data() + base;
+  auto mul = [](double2 a, double2 b2) {
+    return make_double2(a.x * b2.x - a.y * b2.y, a.x * b2.y + a.y * b2.x);
+  };
+  for (int c = 0; c < n; ++c) {
+    // column c of the inverse: T x = e_c
+    if (lower) {
+      for (int k = c; k < n; ++k) {
+        double2 acc = make_double2(k == c ? 1.0 : 0.0, 0.0);
+        for (int j = c; j < k; ++j) {
+          const double2 t = mul(D[(size_t)k * n + j], X[(size_t)j * n + c]);
+          acc.x -= t.x;
+          acc.y -= t.y;
+        }
+        X[(size_t)k * n + c] = mul(acc, dinv[s0 + k]);
+      }
+    } else {
+      for (int k = c; k >= 0; --k) {
+        double2 acc = make_double2(k == c ? 1.0 : 0.0, 0.0);
+        for (int j = k + 1; j <= c; ++j) {
+          const double2 t = mul(D[(size_t)k * n + j], X[(size_t)j * n + c]);
+          acc.x -= t.x;
+          acc.y -= t.y;
+        }
+        X[(size_t)k * n + c] = mul(acc, dinv[s0 + k]);
+      }
+    }
+  }
+}
+
+// queue of blocks by dependency level (lower: deps on earlier blocks;
+// upper: on later ones), and the level count
+std::vector<int> block_queue(const std::vector<int64_t>& ptr, const std::vector<int>& col,
+                             const std::vector<int>& bstart, const std::vector<int>& blen,
+                             const std::vector<int>& bid, bool lower, int32_t* nlev) {
+  const int nb = (int)bstart.size();
+  std::vector<int> lev(nb, 0);
+  for (int t = 0; t < nb; ++t) {
+    const int b2 = lower ? t : nb - 1 - t;
+    int lv = 0;
+    for (int64_t i = bstart[b2]; i < bstart[b2] + blen[b2]; ++i)
+      for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+        const int o = bid[col[e]];
+        if (o != b2) lv = std::max(lv, lev[o] + 1);
+      }
+    lev[b2] = lv;
+  }
+  return level_order(lev, nlev);
+}
+
 int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) {
   const int e = h->epoch;
   count_launch();
+  if (h->blocked) {
+    k_trsv_block<<<h->bgrid, TRSV_BLOCK_THREADS, 0, s>>>(
+        lower ? h->l_border : h->u_border, h->bstart, h->blen, lower ? h->l_boff : h->u_boff,
+        lower ? h->l_binv : h->u_binv, h->nblocks, lower ? h->l_ptr : h->u_ptr,
+        lower ? h->l_col : h->u_col, lower ? h->l_val : h->u_val, b, x,
+        h->flag + (lower ? 0 : h->rows), e, h->head + (lower ? 0 : 1), h->spin_ns);
+    LCK(cudaGetLastError());
+    return 0;
+  }
   k_trsv<<<h->grid, 1024, 0, s>>>(lower ? h->l_order : h->u_order, (int)h->rows,
                                   lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col,
                                   lower ? h->l_val : h->u_val, lower ? h->l_dinv : h->u_dinv, b, x,
@@ -344,6 +484,8 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   h->device = device;
   h->n_layers = n_layers;
   std::vector<int64_t> lptr{0}, uptr{0}, qin, qout;
+  std::vector<int> bstart, blen;  // dissection blocks (global rows), when every layer has them
+  bool blocked = true;
   std::vector<int> lcol, ucol, llev, ulev;
   std::vector<double2> lval, uval, ldinv, udinv;
   int64_t row0 = 0, u_row0 = 0;
@@ -372,6 +514,21 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
       return rc;
     if ((rc = split_factor(A.u_ptr, A.u_col, A.u_val, A.dim, row0, false, uptr, ucol, uval, udinv, ulev)))
       return rc;
+    if (A.n_blocks > 0 && A.block_ptr) {
+      if (A.block_ptr[0] != 0 || A.block_ptr[A.n_blocks] != A.dim)
+        return lfail(PT_EINVAL, "dissection blocks do not cover the layer");
+      for (int64_t k = 0; k < A.n_blocks; ++k) {
+        const int64_t n = A.block_ptr[k + 1] - A.block_ptr[k];
+        if (n < 1 || n > TRSV_BLOCK_MAX) {
+          blocked = false;  // a block the kernel cannot stage: row solve instead
+          break;
+        }
+        bstart.push_back((int)(row0 + A.block_ptr[k]));
+        blen.push_back((int)n);
+      }
+    } else {
+      blocked = false;
+    }
     for (int64_t k = 0; k < A.dim; ++k) {
       if (A.q_in[k] < 0 || A.q_in[k] >= A.dim || A.q_out[k] < 0 || A.q_out[k] >= A.dim)
         return lfail(PT_EINVAL, "local permutation out of range");
@@ -387,12 +544,36 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   h->nxe = nxe;
   h->factor_nnz = (int64_t)lval.size() + (int64_t)uval.size() + 2 * row0;
   std::vector<int> lord = level_order(llev, &h->l_levels), uord = level_order(ulev, &h->u_levels);
+  if (const char* e = std::getenv("PT_TRSV_BLOCK")) blocked = blocked && std::atoi(e) != 0;
+  std::vector<int> lbord, ubord;
+  std::vector<int64_t> lboff, uboff;
+  std::vector<double2> lbinv, ubinv;
+  if (blocked) {
+    std::vector<int> bid(row0, -1);
+    for (size_t k = 0; k < bstart.size(); ++k)
+      for (int i = 0; i < blen[k]; ++i) bid[bstart[k] + i] = (int)k;
+    for (size_t k = 0; k < bstart.size(); ++k) {
+      lboff.push_back((int64_t)lbinv.size());
+      invert_block(lptr, lcol, lval, ldinv, bstart[k], blen[k], true, lbinv);
+      uboff.push_back((int64_t)ubinv.size());
+      invert_block(uptr, ucol, uval, udinv, bstart[k], blen[k], false, ubinv);
+    }
+    lbord = block_queue(lptr, lcol, bstart, blen, bid, true, &h->l_blevels);
+    ubord = block_queue(uptr, ucol, bstart, blen, bid, false, &h->u_blevels);
+    h->nblocks = (int)bstart.size();
+  }
+  h->blocked = blocked;
   int rc;
   if ((rc = up(&h->layers, h->host_layers)) || (rc = up(&h->l_ptr, lptr)) || (rc = up(&h->u_ptr, uptr)) ||
       (rc = up(&h->l_col, lcol)) || (rc = up(&h->u_col, ucol)) || (rc = up(&h->l_val, lval)) ||
       (rc = up(&h->u_val, uval)) || (rc = up(&h->l_dinv, ldinv)) || (rc = up(&h->u_dinv, udinv)) ||
       (rc = up(&h->l_order, lord)) || (rc = up(&h->u_order, uord)) || (rc = up(&h->q_in, qin)) ||
       (rc = up(&h->q_out, qout)))
+    return rc;
+  if (blocked &&
+      ((rc = up(&h->bstart, bstart)) || (rc = up(&h->blen, blen)) || (rc = up(&h->l_border, lbord)) ||
+       (rc = up(&h->u_border, ubord)) || (rc = up(&h->l_boff, lboff)) || (rc = up(&h->u_boff, uboff)) ||
+       (rc = up(&h->l_binv, lbinv)) || (rc = up(&h->u_binv, ubinv))))
     return rc;
   LCK(cudaMalloc(&h->y, row0 * sizeof(double2)));
   LCK(cudaMalloc(&h->w, row0 * sizeof(double2)));
@@ -408,6 +589,9 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   if (const char* e = std::getenv("PT_TRSV_SPIN")) h->spin_ns = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PT_TRSV_CHUNK")) h->chunk = std::max(1, std::atoi(e));
   h->grid = nsm * per_sm;  // every warp resident: spinning warps never block a producer
+  int bocc = 0;
+  LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_trsv_block, TRSV_BLOCK_THREADS, 0));
+  h->bgrid = nsm * std::max(bocc, 1);  // all resident: a waiting block never blocks its producers
   cudaSetDevice(prev);
   *out = h.release();
   return 0;
@@ -429,8 +613,8 @@ int pt_local_info(const pt_local* h, int64_t* rows, int64_t* factor_nnz, int32_t
   if (!h) return lfail(PT_EINVAL, "null handle");
   if (rows) *rows = h->rows;
   if (factor_nnz) *factor_nnz = h->factor_nnz;
-  if (l_levels) *l_levels = h->l_levels;
-  if (u_levels) *u_levels = h->u_levels;
+  if (l_levels) *l_levels = h->blocked ? h->l_blevels : h->l_levels;
+  if (u_levels) *u_levels = h->blocked ? h->u_blevels : h->u_levels;
   return 0;
 }
 

@@ -49,12 +49,16 @@ class DeviceLocalSolver:
                 "q_in": np.ascontiguousarray(f["q_in"], dtype=np.int64),
                 "q_out": np.ascontiguousarray(f["q_out"], dtype=np.int64),
             }
+            bp = f.get("block_ptr")
+            if bp is not None:
+                parts["block_ptr"] = np.ascontiguousarray(bp, dtype=np.int64)
             keep.append(parts)
             a = arr[i]
             a.dim = f["nze"] * f["nxe"]
             a.nze, a.nxe, a.n_layer, a.n_pml = f["nze"], f["nxe"], f["n_layer"], f["n_pml"]
             for k, v in parts.items():
                 setattr(a, k, v.ctypes.data)
+            a.n_blocks = 0 if bp is None else len(bp) - 1
         h = C.c_void_p()
         rc = nat.lib().pt_local_create(arr, self.L, self.device, C.byref(h))
         if rc != 0:
@@ -64,7 +68,8 @@ class DeviceLocalSolver:
         rows, nnz, ll, ul = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
         nat.lib().pt_local_info(self._h, C.byref(rows), C.byref(nnz), C.byref(ll), C.byref(ul))
         self.info = {"rows": rows.value, "factor_nnz": nnz.value, "l_levels": ll.value,
-                     "u_levels": ul.value}
+                     "u_levels": ul.value,
+                     "blocked": all(f.get("block_ptr") is not None for f in factors)}
 
     @classmethod
     def from_config(cls, name, device=None, workers=None):

@@ -13,7 +13,10 @@ residuals ~1e-13 are checked):
     P A P^T = A',   Pr A' Pc = L U   (SuperLU, permc NATURAL on A')
 
 so  A x = b  is  y = b[q_in],  L w = y,  U z = w,  x = z[q_out]  with
-q_in = p[perm_r^-1] and q_out = perm_c[p^-1].
+q_in = p[perm_r^-1] and q_out = perm_c[p^-1].  With diagonal pivoting
+SuperLU keeps the order (perm_r = perm_c = identity, checked), so every leaf
+block and separator of the dissection is a contiguous run of factor rows;
+their offsets (``block_ptr``) let the device solve a whole block at once.
 """
 
 from __future__ import annotations
@@ -31,10 +34,13 @@ from .layers import edge_extend, equal_partition, layer_operator
 __all__ = ["nd_order", "factor_layer", "build_local", "apply_factors"]
 
 
-def nd_order(nze, nxe, min_block=4):
+def nd_order(nze, nxe, min_block=4, blocks=False):
     """Geometric nested dissection of the nze x nxe grid (index z * nxe + x):
-    split the longer side by a grid line, order both halves, then the line."""
+    split the longer side by a grid line, order both halves, then the line.
+    ``blocks=True`` also returns the start offsets of the leaf blocks and
+    separators in the order (plus the total), each a contiguous run."""
     out = []
+    starts = []
     stack = [(0, nze, 0, nxe, False)]
     # iterative post-order: (region, emitted-children flag)
     while stack:
@@ -43,11 +49,13 @@ def nd_order(nze, nxe, min_block=4):
         if w <= 0 or hgt <= 0:
             continue
         if w * hgt <= min_block * min_block or (w <= 2 and hgt <= 2):
+            starts.append(len(out))
             out.extend(z * nxe + x for z in range(z0, z1) for x in range(x0, x1))
             continue
         if w >= hgt:
             xm = (x0 + x1) // 2
             if done:
+                starts.append(len(out))
                 out.extend(z * nxe + xm for z in range(z0, z1))
                 continue
             stack.append((z0, z1, x0, x1, True))
@@ -56,6 +64,7 @@ def nd_order(nze, nxe, min_block=4):
         else:
             zm = (z0 + z1) // 2
             if done:
+                starts.append(len(out))
                 out.extend(zm * nxe + x for x in range(x0, x1))
                 continue
             stack.append((z0, z1, x0, x1, True))
@@ -64,6 +73,8 @@ def nd_order(nze, nxe, min_block=4):
     p = np.asarray(out, dtype=np.int64)
     if p.size != nze * nxe or np.unique(p).size != p.size:
         raise AssertionError("nested-dissection order is not a permutation")
+    if blocks:
+        return p, np.asarray(starts + [len(out)], dtype=np.int64)
     return p
 
 
@@ -71,16 +82,19 @@ def factor_layer(op, nze, nxe, check=True):
     """Factor one layer operator for the device: dict of CSR L, U and the
     composed gathers q_in / q_out (see the module docstring)."""
     op = sp.csc_matrix(op)
-    p = nd_order(nze, nxe)
+    p, blocks = nd_order(nze, nxe, blocks=True)
     a = sp.csc_matrix(op[p][:, p])
     lu = spla.splu(a, permc_spec="NATURAL", diag_pivot_thresh=0.0)
+    ident = np.arange(a.shape[0])
+    if not (np.array_equal(lu.perm_r, ident) and np.array_equal(lu.perm_c, ident)):
+        blocks = None  # SuperLU reordered: the blocks are no longer contiguous runs
     L, U = lu.L.tocsr(), lu.U.tocsr()
     L.sort_indices()
     U.sort_indices()
     inv_pr = np.argsort(lu.perm_r)
     inv_p = np.argsort(p)
     fac = {"L": L, "U": U, "q_in": p[inv_pr].astype(np.int64),
-           "q_out": np.asarray(lu.perm_c, dtype=np.int64)[inv_p]}
+           "q_out": np.asarray(lu.perm_c, dtype=np.int64)[inv_p], "block_ptr": blocks}
     if check:
         rng = np.random.default_rng(0)
         b = rng.standard_normal(op.shape[0]) + 1j * rng.standard_normal(op.shape[0])

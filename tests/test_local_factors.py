@@ -66,3 +66,18 @@ def test_factor_layer_residual_and_levels():
     b = rng.standard_normal(op.shape[0]) + 1j * rng.standard_normal(op.shape[0])
     assert np.linalg.norm(op @ apply_factors(fac, b) - b) <= 1e-12 * np.linalg.norm(b)
     assert np.allclose(fac["L"].diagonal(), 1.0)
+
+
+def test_nd_blocks_are_contiguous_runs_of_the_factor():
+    """The dissection blocks handed to the device: contiguous, covering, and
+    SuperLU kept the order (so each block's diagonal block is triangular)."""
+    p, starts = nd_order(12, 40, blocks=True)
+    assert starts[0] == 0 and starts[-1] == p.size and np.all(np.diff(starts) > 0)
+    facs, geo = build_local("fx_plr", workers=1)
+    for fac in facs:
+        bp = fac["block_ptr"]
+        assert bp is not None and bp[-1] == fac["L"].shape[0]
+        # no entry of L couples a row to a LATER block (lower triangular by blocks)
+        L = fac["L"].tocoo()
+        blk = np.searchsorted(bp, np.arange(L.shape[0]), side="right") - 1
+        assert np.all(blk[L.col] <= blk[L.row])
