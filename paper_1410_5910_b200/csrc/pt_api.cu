@@ -537,12 +537,16 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
   }
   for (int s : {SLOT_Y, SLOT_U1, SLOT_U2, SLOT_PRE, SLOT_T})
     if ((rc = ensure_slot(h, s, p->host.slot_elems[s]))) return rc;
-  if (p->host.n_counters + 1 > h->ctr_cap) {
+  // counters + queue head + exit ticket; zero between launches (the
+  // executor's last CTA resets them)
+  if (p->host.n_counters + 2 > h->ctr_cap) {
     CK(cudaDeviceSynchronize());
     h->drop_graphs();
     cudaFree(h->ctr);
-    h->ctr_cap = p->host.n_counters + 1;
+    h->ctr_cap = p->host.n_counters + 2;
     CK(cudaMalloc(&h->ctr, h->ctr_cap * sizeof(int)));
+    CK(cudaMemset(h->ctr, 0, h->ctr_cap * sizeof(int)));
+    CK(cudaDeviceSynchronize());
   }
   *out = p.get();
   h->progs[key] = std::move(p);
@@ -596,7 +600,6 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.vbase = im.vbase;
   a.vstride = im.vstride;
   a.trace = h->trace_buf;
-  CK(cudaMemsetAsync(h->ctr, 0, (p->host.n_counters + 1) * sizeof(int), s));
   count_launch();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->timing) {
@@ -1171,7 +1174,11 @@ int gmres_stream(pt_handle* h, const double2* b, double2* x, const pt_gmres_conf
   const int64_t N = h->N();
   if ((rc = run_program(h, pM, b, d.V, nullptr, s))) return rc;
   gm_begin(d, 0, s);
-  const int B = 2;
+  // per-launch timing: one iteration per batch and no speculative launches
+  // (a launch after the stop returns at once but would still be counted with
+  // its program's bytes)
+  const bool ahead = !h->timing;
+  const int B = ahead ? 2 : 1;
   int enq = 0, nb = 0, waited = 0;
   DevStatus last{};
   IterMode im;
@@ -1191,11 +1198,15 @@ int gmres_stream(pt_handle* h, const double2* b, double2* x, const pt_gmres_conf
   };
   if ((rc = enqueue_batch())) return rc;
   for (;;) {
-    if (enq < cfg->max_iter && (rc = enqueue_batch())) return rc;
+    if (ahead && enq < cfg->max_iter && (rc = enqueue_batch())) return rc;
     CK(cudaEventSynchronize(w->ev[waited % 2]));
     last = w->st_host[waited % 2];
     ++waited;
     if (last.stop) break;
+    if (!ahead && enq < cfg->max_iter) {
+      if ((rc = enqueue_batch())) return rc;
+      continue;
+    }
     if (waited == nb && enq >= cfg->max_iter) break;
   }
   gm_finish(d, x, s);
@@ -1429,8 +1440,10 @@ int bgmres_run(pt_handle* h, const pt_gmres_config* cfg, int nrhs, cudaStream_t 
     if ((rc = run_bprogram(h, pM, B.b, g.V, s))) return rc;
     bg_begin(g, 0, s);
     int enq = 0, nb = 0, waited = 0;
+    // per-launch timing: no speculative launches (see gmres_stream)
+    const bool ahead = !h->timing;
     auto enqueue = [&]() -> int {
-      for (int i = 0; i < 2 && enq < cfg->max_iter; ++i, ++enq) {
+      for (int i = 0; i < (ahead ? 2 : 1) && enq < cfg->max_iter; ++i, ++enq) {
         int r = run_bprogram(h, pAM, nullptr, nullptr, s, g.ctl + 1, g.ctl, g.V, vstride);
         if (r) return r;
         bg_step(g, cfg->rel_tol, cfg->max_iter, 0, s);
@@ -1442,11 +1455,15 @@ int bgmres_run(pt_handle* h, const pt_gmres_config* cfg, int nrhs, cudaStream_t 
     };
     if ((rc = enqueue())) return rc;
     for (;;) {
-      if (enq < cfg->max_iter && (rc = enqueue())) return rc;
+      if (ahead && enq < cfg->max_iter && (rc = enqueue())) return rc;
       CK(cudaEventSynchronize(B.ev[waited % 2]));
       const int stop = B.ctl_host[4 * (waited % 2) + 1];
       ++waited;
       if (stop) break;
+      if (!ahead && enq < cfg->max_iter) {
+        if ((rc = enqueue())) return rc;
+        continue;
+      }
       if (waited == nb && enq >= cfg->max_iter) break;
     }
     if ((rc = epilogue(s))) return rc;

@@ -719,9 +719,25 @@ __global__ void __launch_bounds__(EXEC_THREADS, 512 / EXEC_CONSUMERS) pt_exec_ke
   const Layout L = carve(smem, a);
   if (threadIdx.x >= CONSUMERS) {
     const int k = (threadIdx.x - CONSUMERS) >> 5;
-    if (k < L.n_slots) producer(a, L, k);  // unused task slots: their warps retire
+    if (k < L.n_slots) producer(a, L, k);  // unused task slots: their warps wait below
   } else {
     consumer(a, L);
+  }
+  // Counters reset themselves: the last CTA out zeroes the program's
+  // counters, the queue head and the exit ticket, so the next launch needs
+  // no memset node (a memset between two kernels cost ~11 us of launch gap
+  // per GMRES iteration).  Every CTA's polls and signals are done here.
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.head + 1, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int n = (int)(a.head - a.ctr) + 2;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) a.ctr[i] = 0;
   }
 }
 

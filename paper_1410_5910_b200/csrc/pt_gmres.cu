@@ -16,6 +16,9 @@
 // kernels reduce partials in the last block to finish (ticket counter).  Every step kernel returns at
 // once when the status says the solve has stopped: the host enqueues steps
 // ahead of its convergence check without changing the result.
+#ifdef PT_ARN_PROFILE
+#include <cstdio>
+#endif
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -106,10 +109,26 @@ __device__ void reduce_partials(const double2* P, int ldp, int ncols, double2* o
 
 __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 
+// Operands of the Givens update, gathered into shared memory by block 0 of
+// the Arnoldi step while the reductions run: the one-thread rotation chain
+// then reads no global memory (a global load per rotation, ordered behind
+// the previous rotation's stores, cost ~0.4 us each: 14 us at j = 35).
+struct GivensSmem {
+  double2* h1;  // CGS pass-1 coefficients, rows 0..j
+  double2* h2;  // pass 2
+  double2* cs;  // rotation cosines in .x, rows 0..j-1
+  double2* sn;  // rotation sines
+  double2 gj;   // g[j]
+  double beta;
+  double hist_w;  // hist[k - 1 - STAG_WINDOW] (k > STAG_WINDOW)
+  int nonfinite;
+};
+
 // Arnoldi column j: h = h1 + h2, hn; rotations; residual; flags (one thread)
-__device__ void givens_update(const GmresDev& g, int j, double rel_tol, int max_iter) {
+__device__ __noinline__ void givens_update(const GmresDev& g, const GivensSmem& q, int j, double hn,
+                              double rel_tol, int max_iter) {
   DevStatus* st = g.st;
-  if (*((volatile int*)g.nonfinite)) {
+  if (q.nonfinite) {
     st->nonfinite = 1;
     st->stop = 1;
     st->converged = 0;
@@ -118,20 +137,17 @@ __device__ void givens_update(const GmresDev& g, int j, double rel_tol, int max_
   const int ldr = g.max_iter + 1;
   double2* Rj = g.R + (int64_t)j * ldr;
   double2* Hj = g.Hraw + (int64_t)j * ldr;
-  const double hn = sqrt(ld_cg(g.hn2).x);
   Hj[j + 1] = make_double2(hn, 0.0);
   // previous rotations down the new column; the running entry is carried in
-  // registers and every load (h, cs, sn) is independent of the rotation
-  // chain, so only the FMA chain is serial (a store/load round trip per
-  // rotation through memory would cost ~1 us each)
-  double2 a = cadd(ld_cg(g.h1), ld_cg(g.h2));
+  // registers, the operands come from shared memory
+  double2 a = cadd(q.h1[0], q.h2[0]);
   Hj[0] = a;
 #pragma unroll 4
   for (int i = 0; i < j; ++i) {
-    const double2 b = cadd(ld_cg(g.h1 + i + 1), ld_cg(g.h2 + i + 1));
+    const double2 b = cadd(q.h1[i + 1], q.h2[i + 1]);
     Hj[i + 1] = b;
-    const double c = g.cs[i];
-    const double2 s = g.sn[i];
+    const double c = q.cs[i].x;
+    const double2 s = q.sn[i];
     Rj[i] = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
     a = cadd(cmul(make_double2(-s.x, s.y), a), make_double2(c * b.x, c * b.y));
   }
@@ -158,11 +174,12 @@ __device__ void givens_update(const GmresDev& g, int j, double rel_tol, int max_
   g.sn[j] = s;
   Rj[j] = rr;
   Rj[j + 1] = make_double2(0.0, 0.0);
-  const double2 gj = g.g[j];
+  const double2 gj = q.gj;
+  const double2 gj1 = cmul(make_double2(-s.x, s.y), gj);
   g.g[j] = make_double2(c * gj.x, c * gj.y);
-  g.g[j + 1] = cmul(make_double2(-s.x, s.y), gj);
-  const double beta = st->beta;
-  const double rel = sqrt(cabs2(g.g[j + 1])) / beta;
+  g.g[j + 1] = gj1;
+  const double beta = q.beta;
+  const double rel = sqrt(cabs2(gj1)) / beta;
   g.hist[j] = rel;
   const int k = j + 1;
   st->iterations = k;
@@ -180,37 +197,51 @@ __device__ void givens_update(const GmresDev& g, int j, double rel_tol, int max_
     st->flag = 0;
     st->stop = 1;
   } else if (k > STAG_WINDOW &&  // solver.py:282-287
-             g.hist[k - 1 - STAG_WINDOW] > 0.0 &&
-             1.0 - rel / g.hist[k - 1 - STAG_WINDOW] < STAG_IMPROVEMENT) {
+             q.hist_w > 0.0 && 1.0 - rel / q.hist_w < STAG_IMPROVEMENT) {
     st->flag = 2;
     st->stop = 1;
   } else if (k >= max_iter) {  // for/else, solver.py:288-289
     st->flag = 3;
     st->stop = 1;
   }
-  __threadfence();
 }
 
 // ---- fused Arnoldi step ---------------------------------------------------------
 
+// phase timestamps of the Arnoldi step (profiling build only: -DPT_ARN_PROFILE,
+// tools/arn_phases.sh); block 0 and the last block print the phase deltas
+#ifdef PT_ARN_PROFILE
+#define ARN_MARK(i) \
+  do {                                                                        \
+    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm[i])); \
+  } while (0)
+#else
+#define ARN_MARK(i) \
+  do {            \
+  } while (0)
+#endif
+
 namespace cg = cooperative_groups;
 
-// out[c] = sum over blocks b (index order) of P[b * ldp + c], c < nc, by
-// groups of 8 threads per column (partials b = sub mod 8 in order, then a
-// fixed xor tree): the same result in every block
+// out[c] = sum over blocks b of P[b * ldp + c], c < nc: a warp per column,
+// lane l sums partials b = l, l + 32, ... in order (all loads issued before
+// the adds: the L2 latency is paid once, not once per partial), then a fixed
+// xor tree -- the same result in every block
 __device__ void arn_reduce(const double2* P, int ldp, int nblk, int nc, double2* out) {
-  const int sub = threadIdx.x & 7;
-  for (int c0 = 0; c0 < nc; c0 += ARN_THREADS / 8) {
-    const int c = c0 + (int)threadIdx.x / 8;
-    double2 s = make_double2(0.0, 0.0);
-    if (c < nc)
-      for (int b = sub; b < nblk; b += 8) s = cadd(s, ld_cg(P + (int64_t)b * ldp + c));
+  constexpr int PER = (ARN_MAX_BLOCKS + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  for (int c = (int)threadIdx.x >> 5; c < nc; c += ARN_THREADS / 32) {
+    double2 v[PER];
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    for (int i = 0; i < PER; ++i) {
+      const int b = lane + 32 * i;
+      v[i] = b < nblk ? ld_cg(P + (int64_t)b * ldp + c) : make_double2(0.0, 0.0);
     }
-    if (c < nc && sub == 0) out[c] = s;
+    double2 s = v[0];
+#pragma unroll
+    for (int i = 1; i < PER; ++i) s = cadd(s, v[i]);
+    s = warp_sum(s);
+    if (lane == 0) out[c] = s;
   }
 }
 
@@ -223,6 +254,7 @@ __device__ void arn_dots(const double2* Vb, int64_t ldb, int nc, const double2* 
   for (int c = warp; c < nc; c += ARN_THREADS / 32) {
     const double2* v = Vb + (int64_t)c * ldb;
     double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
     for (int e = lane; e < len; e += 32) acc = cfma_conj(v[e], ws[e], acc);  // generic: smem or global
     acc = warp_sum(acc);
     if (lane == 0) st_cg(Prow + c, acc);
@@ -234,6 +266,7 @@ __device__ void arn_update(const double2* Vb, int64_t ldb, int nc, const double2
                            int len) {
   for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
     double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
     for (int c = 0; c < nc; ++c) acc = cfma(Vb[(int64_t)c * ldb + e], h[c], acc);
     ws[e] = csub(ws[e], acc);
   }
@@ -245,6 +278,10 @@ __global__ void __launch_bounds__(ARN_THREADS, 1)
 k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle cond) {
   extern __shared__ double2 sm[];
   if (stopped(g.st)) return;  // uniform: no block reaches a grid barrier
+#ifdef PT_ARN_PROFILE
+  unsigned long long tm[10] = {0};
+#endif
+  ARN_MARK(0);
   cg::grid_group grid = cg::this_grid();
   const int j = g.st->iterations;
   const int nc = j + 1;
@@ -253,7 +290,14 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
   const int64_t lo = (int64_t)blockIdx.x * chunk;
   const int len = (int)(lo + chunk < g.n ? chunk : (lo < g.n ? g.n - lo : 0));
   double2* hsm = sm;                  // coefficients (ldp)
-  double2* ws = sm + g.ldp;           // the block's slice of w
+  __shared__ GivensSmem gq;           // block 0: the Givens update's operands
+  if (threadIdx.x == 0) {
+    gq.h1 = sm + g.ldp;
+    gq.h2 = sm + 2 * g.ldp;
+    gq.cs = sm + 3 * g.ldp;
+    gq.sn = sm + 4 * g.ldp;
+  }
+  double2* ws = sm + ARN_SMEM_VECS * g.ldp;  // the block's slice of w
   double2* vs = ws + chunk;           // the block's slice of V[:, 0..j] (when it fits)
   double2* w = g.V + (int64_t)(j + 1) * g.n;
   double2* P1 = g.P;
@@ -287,6 +331,17 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
           "l"(g.V + (int64_t)c * g.n + lo), "r"((uint32_t)(len * sizeof(double2))),
           "r"((uint32_t)__cvta_generic_to_shared(&s_vbar))
           : "memory");
+  if (blockIdx.x == 0) {  // Givens operands from earlier iterations (off the critical path)
+    for (int i = threadIdx.x; i < j; i += ARN_THREADS) {
+      sm[3 * g.ldp + i] = make_double2(g.cs[i], 0.0);
+      sm[4 * g.ldp + i] = g.sn[i];
+    }
+    if (threadIdx.x == 32) {
+      gq.gj = g.g[j];
+      gq.beta = g.st->beta;
+      gq.hist_w = j + 1 > STAG_WINDOW ? g.hist[j - STAG_WINDOW] : 0.0;
+    }
+  }
   int bad = 0;
   for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
     const double2 v = ld_cg(w + lo + e);
@@ -306,23 +361,36 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
           : "r"((uint32_t)__cvta_generic_to_shared(&s_vbar))
           : "memory");
   }
+  ARN_MARK(1);
   // pass 1: h1 = V^H w
   arn_dots(Vb, ldb, nc, ws, len, P1 + (int64_t)blockIdx.x * g.ldp);
+  ARN_MARK(2);
   grid.sync();
+  ARN_MARK(3);
+  // every block's non-finite flag is set before the first barrier
+  if (blockIdx.x == 0 && threadIdx.x == 32) gq.nonfinite = *((volatile int*)g.nonfinite);
   arn_reduce(P1, g.ldp, nblk, nc, hsm);
   __syncthreads();
   if (blockIdx.x == 0)
-    for (int c = threadIdx.x; c < nc; c += ARN_THREADS) st_cg(g.h1 + c, hsm[c]);
+    for (int c = threadIdx.x; c < nc; c += ARN_THREADS) {
+      st_cg(g.h1 + c, hsm[c]);
+      sm[g.ldp + c] = hsm[c];
+    }
   __syncthreads();
   // pass 2: w -= V h1, h2 = V^H w
   arn_update(Vb, ldb, nc, hsm, ws, len);
   __syncthreads();
   arn_dots(Vb, ldb, nc, ws, len, P2 + (int64_t)blockIdx.x * g.ldp);
+  ARN_MARK(4);
   grid.sync();
+  ARN_MARK(5);
   arn_reduce(P2, g.ldp, nblk, nc, hsm);
   __syncthreads();
   if (blockIdx.x == 0)
-    for (int c = threadIdx.x; c < nc; c += ARN_THREADS) st_cg(g.h2 + c, hsm[c]);
+    for (int c = threadIdx.x; c < nc; c += ARN_THREADS) {
+      st_cg(g.h2 + c, hsm[c]);
+      sm[2 * g.ldp + c] = hsm[c];
+    }
   __syncthreads();
   // w -= V h2, ||w||^2
   arn_update(Vb, ldb, nc, hsm, ws, len);
@@ -343,16 +411,18 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
       st_cg(P1 + (int64_t)blockIdx.x * g.ldp, s);  // P1 is free: pass-1 partials consumed
     }
   }
+  ARN_MARK(6);
   grid.sync();
+  ARN_MARK(7);
   arn_reduce(P1, g.ldp, nblk, 1, hsm);
   __syncthreads();
   const double hn = sqrt(hsm[0].x);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st_cg(g.hn2, hsm[0]);
-    __threadfence();
-    givens_update(g, j, rel_tol, max_iter);
+    givens_update(g, gq, j, hn, rel_tol, max_iter);
     if (cond) cudaGraphSetConditional(cond, g.st->stop ? 0u : 1u);
   }
+  ARN_MARK(8);
   // v_{j+1} = w / ||w|| (unused when the solve stops here; breakdown => 0)
   const double inv = hn <= BREAKDOWN_REL * g.st->beta ? 0.0 : 1.0 / hn;
   for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
@@ -361,6 +431,15 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
     v.y *= inv;
     st_cg(w + lo + e, v);
   }
+  ARN_MARK(9);
+#ifdef PT_ARN_PROFILE
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("ARN j=%d blk=%d stage %llu dots1 %llu sync1 %llu red+upd+dots2 %llu sync2 %llu "
+           "red+upd+norm %llu sync3 %llu red+givens %llu normalize %llu total %llu\n",
+           j, blockIdx.x, tm[1] - tm[0], tm[2] - tm[1], tm[3] - tm[2], tm[4] - tm[3],
+           tm[5] - tm[4], tm[6] - tm[5], tm[7] - tm[6], tm[8] - tm[7], tm[9] - tm[8],
+           tm[9] - tm[0]);
+#endif
 }
 
 // ---- kernels -----------------------------------------------------------------
@@ -498,7 +577,7 @@ int grid_for(int64_t n) {
 cudaError_t gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
                             cudaGraphConditionalHandle cond, cudaStream_t s) {
   const int64_t chunk = (g.n + g.arn_blocks - 1) / g.arn_blocks;
-  const size_t smem = (size_t)(g.ldp + chunk + g.arn_vcap) * sizeof(double2);
+  const size_t smem = (size_t)(ARN_SMEM_VECS * g.ldp + chunk + g.arn_vcap) * sizeof(double2);
   count_launch();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.arn_blocks);
@@ -522,7 +601,7 @@ cudaError_t gm_arnoldi_setup(GmresDev& g, int device) {
   int maxdyn = 0;
   e = cudaDeviceGetAttribute(&maxdyn, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (e != cudaSuccess) return e;
-  const int64_t fixed = (int64_t)(g.ldp + chunk) * (int64_t)sizeof(double2);
+  const int64_t fixed = (int64_t)(ARN_SMEM_VECS * g.ldp + chunk) * (int64_t)sizeof(double2);
   g.arn_vcap = std::max<int64_t>(0, (maxdyn - 1024 - fixed) / (int64_t)sizeof(double2));
   const size_t smem = (size_t)fixed + (size_t)g.arn_vcap * sizeof(double2);
   // per-function attribute shared by every workspace: it only grows

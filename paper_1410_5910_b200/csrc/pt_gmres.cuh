@@ -10,6 +10,7 @@ constexpr int RED_BLOCKS = 296;  // fixed partial count => deterministic sums
 constexpr int RED_CHUNK = 8;     // basis columns per pass of the dot kernel
 constexpr int ARN_THREADS = 512; // fused Arnoldi step: threads per block
 constexpr int ARN_MAX_BLOCKS = RED_BLOCKS;
+constexpr int ARN_SMEM_VECS = 5;   // Arnoldi step: coefficients + Givens operands (ldp each)
 
 // STAGNATION_WINDOW / STAGNATION_IMPROVEMENT of solver.py:55-56
 constexpr int STAG_WINDOW = 10;
