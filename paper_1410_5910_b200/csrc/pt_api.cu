@@ -60,7 +60,10 @@ struct DevProgram {
   DevItem* items = nullptr;
   int4* blob = nullptr;        // per-task metadata blobs (queue order)
   int64_t* blob_off = nullptr;  // task q: blob[blob_off[q] .. blob_off[q + 1])
+  int* qlist = nullptr;         // split queues (chain_ctas > 0): other tasks, then chain tasks
+  int qlen[2] = {0, 0};
   ~DevProgram() {
+    cudaFree(qlist);
     cudaFree(blob);
     cudaFree(blob_off);
     cudaFree(ents);
@@ -144,6 +147,7 @@ struct pt_handle {
   int n_slots = EXEC_TSLOTS;  // task slots in use per CTA
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
   int poll_stagger = 0;    // staggered polling of few counters (PT_POLL_STAGGER cycles; 0: off)
+  int chain_ctas = 0;      // CTAs reserved for the sweep-chain tasks (PT_CHAIN_CTAS; 0: one queue)
   std::unique_ptr<pt_gmres_ws> gws;
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
@@ -537,13 +541,24 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
   }
   for (int s : {SLOT_Y, SLOT_U1, SLOT_U2, SLOT_PRE, SLOT_T})
     if ((rc = ensure_slot(h, s, p->host.slot_elems[s]))) return rc;
-  // counters + queue head + exit ticket; zero between launches (the
-  // executor's last CTA resets them)
-  if (p->host.n_counters + 2 > h->ctr_cap) {
+  if (h->chain_ctas > 0) {  // split queues: the sweep-chain tasks on their own CTAs
+    std::vector<int> other, chain;
+    for (size_t q = 0; q < p->host.tasks.size(); ++q)
+      (p->host.chain[q] ? chain : other).push_back((int)q);
+    if (!chain.empty() && !other.empty()) {
+      p->qlen[0] = (int)other.size();
+      p->qlen[1] = (int)chain.size();
+      other.insert(other.end(), chain.begin(), chain.end());
+      if ((rc = upload(&p->qlist, other))) return rc;
+    }
+  }
+  // counters + queue head + exit ticket + chain queue head; zero between
+  // launches (the executor's last CTA resets them)
+  if (p->host.n_counters + 3 > h->ctr_cap) {
     CK(cudaDeviceSynchronize());
     h->drop_graphs();
     cudaFree(h->ctr);
-    h->ctr_cap = p->host.n_counters + 2;
+    h->ctr_cap = p->host.n_counters + 3;
     CK(cudaMalloc(&h->ctr, h->ctr_cap * sizeof(int)));
     CK(cudaMemset(h->ctr, 0, h->ctr_cap * sizeof(int)));
     CK(cudaDeviceSynchronize());
@@ -596,6 +611,10 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
   a.stop = stop;
+  a.qlist = p->qlist;
+  a.qlen0 = p->qlen[0];
+  a.qlen1 = p->qlen[1];
+  a.chain_ctas = h->chain_ctas;
   a.iter = im.iter;
   a.vbase = im.vbase;
   a.vstride = im.vstride;
@@ -931,6 +950,8 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_ROW_CHUNK")) h->pp.row_chunk = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_POLL_NS")) h->poll_ns = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PT_POLL_STAGGER")) h->poll_stagger = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("PT_CHAIN_CTAS"))
+    h->chain_ctas = std::min(std::max(0, std::atoi(e)), std::max(0, h->grid - 1));
   if (const char* e = std::getenv("PT_CHAIN_PIECE")) h->pp.chain_piece_elems = std::atoll(e);
   if (const char* e = std::getenv("PT_CHAIN_BOOST")) h->pp.chain_boost_us = std::atof(e);
   if (const char* e = std::getenv("PT_SIM_SLOTS")) h->pp.ctas = h->grid * std::max(1, std::atoi(e));

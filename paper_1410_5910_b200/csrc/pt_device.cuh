@@ -126,6 +126,12 @@ struct ExecArgs {
   unsigned long long* trace;  // optional per-task timeline (debug/profiling)
   int n_tasks;
   int m;
+  // split queues (optional): CTAs [0, chain_ctas) take the sweep-chain tasks
+  // qlist[qlen0 ..), the others the remaining tasks qlist[0 .. qlen0), each
+  // list in queue order; head[0] / head[2] are their grab counters
+  const int* qlist;
+  int qlen0, qlen1;
+  int chain_ctas;
 };
 
 // TMA bulk prefetch of a contiguous range into L2 (no smem, no completion)

@@ -359,7 +359,13 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     int q = 0;
     if (lane == 0) {
       while (s_grab_turn != use) __nanosleep(16);
-      q = atomicAdd(a.head, 1);
+      if (a.qlist) {  // split queues: chain CTAs / the rest
+        const bool ch = (int)blockIdx.x < a.chain_ctas;
+        const int i = atomicAdd(a.head + (ch ? 2 : 0), 1);
+        q = i < (ch ? a.qlen1 : a.qlen0) ? a.qlist[(ch ? a.qlen0 : 0) + i] : a.n_tasks;
+      } else {
+        q = atomicAdd(a.head, 1);
+      }
       s_grab_turn = use + 1;
     }
     q = __shfl_sync(0xffffffffu, q, 0);
@@ -724,7 +730,7 @@ __global__ void __launch_bounds__(EXEC_THREADS, 512 / EXEC_CONSUMERS) pt_exec_ke
     consumer(a, L);
   }
   // Counters reset themselves: the last CTA out zeroes the program's
-  // counters, the queue head and the exit ticket, so the next launch needs
+  // counters, the queue heads and the exit ticket, so the next launch needs
   // no memset node (a memset between two kernels cost ~11 us of launch gap
   // per GMRES iteration).  Every CTA's polls and signals are done here.
   __shared__ int s_last;
@@ -736,7 +742,7 @@ __global__ void __launch_bounds__(EXEC_THREADS, 512 / EXEC_CONSUMERS) pt_exec_ke
   __syncthreads();
   if (s_last) {
     __threadfence();
-    const int n = (int)(a.head - a.ctr) + 2;
+    const int n = (int)(a.head - a.ctr) + 3;
     for (int i = threadIdx.x; i < n; i += blockDim.x) a.ctr[i] = 0;
   }
 }

@@ -406,6 +406,7 @@ class Builder {
         out.waits.push_back(w);
       }
       out.tasks.push_back(tk);
+      out.chain.push_back(task_chain_[idx] ? 1 : 0);
     }
     return out;
   }

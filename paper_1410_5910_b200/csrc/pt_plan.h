@@ -45,6 +45,7 @@ struct Program {
   std::vector<DevItem> items;      // per-task metadata items
   std::vector<DevRun> runs;        // Y_PLR t-value runs
   std::vector<DevSrcRun> sruns;    // Y_PLR dense-leaf source runs
+  std::vector<uint8_t> chain;      // per task (queue order): on a sweep's dependency chain
   int n_counters = 0;
   int64_t t_elems = 0;      // size of SLOT_T needed
   int64_t term_bytes = 0;   // kernel bytes actually streamed by the terms
