@@ -223,11 +223,18 @@ __device__ __noinline__ void givens_update(const GmresDev& g, const GivensSmem& 
 
 namespace cg = cooperative_groups;
 
-// out[c] = sum over blocks b of P[b * ldp + c], c < nc: a warp per column,
-// lane l sums partials b = l, l + 32, ... in order (all loads issued before
-// the adds: the L2 latency is paid once, not once per partial), then a fixed
-// xor tree -- the same result in every block
-__device__ void arn_reduce(const double2* P, int ldp, int nblk, int nc, double2* out) {
+// Partials of the Arnoldi step are stored column-major: the block-b partial
+// of coefficient c is P[c * RED_BLOCKS + b], so the partials of one
+// coefficient are contiguous and a warp reads them with coalesced loads
+// (every block reads every partial: with a row-per-block layout the 148
+// blocks' strided loads queued ~8x more L2 requests on the same lines, and
+// the reduction took 6.8 us at j = 35).
+//
+// out[c] = sum over blocks b of the partials of c, c < nc: a warp per
+// coefficient, lane l sums partials b = l, l + 32, ... in order (all loads
+// issued before the adds), then a fixed xor tree -- the same result in every
+// block
+__device__ void arn_reduce(const double2* P, int nblk, int nc, double2* out) {
   constexpr int PER = (ARN_MAX_BLOCKS + 31) / 32;
   const int lane = threadIdx.x & 31;
   for (int c = (int)threadIdx.x >> 5; c < nc; c += ARN_THREADS / 32) {
@@ -235,7 +242,7 @@ __device__ void arn_reduce(const double2* P, int ldp, int nblk, int nc, double2*
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int b = lane + 32 * i;
-      v[i] = b < nblk ? ld_cg(P + (int64_t)b * ldp + c) : make_double2(0.0, 0.0);
+      v[i] = b < nblk ? ld_cg(P + (int64_t)c * RED_BLOCKS + b) : make_double2(0.0, 0.0);
     }
     double2 s = v[0];
 #pragma unroll
@@ -249,15 +256,21 @@ __device__ void arn_reduce(const double2* P, int ldp, int nblk, int nc, double2*
 // the block's slice of w in shared memory; Vb = element 0 of the slice of
 // column 0, columns ldb apart (global memory, or the slice staged in smem)
 __device__ void arn_dots(const double2* Vb, int64_t ldb, int nc, const double2* ws, int len,
-                         double2* Prow) {
+                         double2* P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c = warp; c < nc; c += ARN_THREADS / 32) {
     const double2* v = Vb + (int64_t)c * ldb;
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (int e = lane; e < len; e += 32) acc = cfma_conj(v[e], ws[e], acc);  // generic: smem or global
-    acc = warp_sum(acc);
-    if (lane == 0) st_cg(Prow + c, acc);
+    // two accumulators (fixed assignment: elements e < len alternate), so the
+    // FP64 FMA latency chain is half as long
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+    int e = lane;
+    for (; e + 32 < len; e += 64) {  // generic: smem or global
+      a0 = cfma_conj(v[e], ws[e], a0);
+      a1 = cfma_conj(v[e + 32], ws[e + 32], a1);
+    }
+    if (e < len) a0 = cfma_conj(v[e], ws[e], a0);
+    double2 acc = warp_sum(cadd(a0, a1));
+    if (lane == 0) st_cg(P + (int64_t)c * RED_BLOCKS + blockIdx.x, acc);
   }
 }
 
@@ -265,10 +278,18 @@ __device__ void arn_dots(const double2* Vb, int64_t ldb, int nc, const double2* 
 __device__ void arn_update(const double2* Vb, int64_t ldb, int nc, const double2* h, double2* ws,
                            int len) {
   for (int e = threadIdx.x; e < len; e += ARN_THREADS) {
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (int c = 0; c < nc; ++c) acc = cfma(Vb[(int64_t)c * ldb + e], h[c], acc);
-    ws[e] = csub(ws[e], acc);
+    // four accumulators over c mod 4 (fixed order of the final sum): the FP64
+    // FMA latency chain is a quarter as long
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+    int c = 0;
+    for (; c + 4 <= nc; c += 4) {
+      a0 = cfma(Vb[(int64_t)c * ldb + e], h[c], a0);
+      a1 = cfma(Vb[(int64_t)(c + 1) * ldb + e], h[c + 1], a1);
+      a2 = cfma(Vb[(int64_t)(c + 2) * ldb + e], h[c + 2], a2);
+      a3 = cfma(Vb[(int64_t)(c + 3) * ldb + e], h[c + 3], a3);
+    }
+    for (; c < nc; ++c) a0 = cfma(Vb[(int64_t)c * ldb + e], h[c], a0);
+    ws[e] = csub(ws[e], cadd(cadd(a0, a1), cadd(a2, a3)));
   }
 }
 
@@ -279,7 +300,7 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
   extern __shared__ double2 sm[];
   if (stopped(g.st)) return;  // uniform: no block reaches a grid barrier
 #ifdef PT_ARN_PROFILE
-  unsigned long long tm[10] = {0};
+  unsigned long long tm[12] = {0};
 #endif
   ARN_MARK(0);
   cg::grid_group grid = cg::this_grid();
@@ -363,13 +384,13 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
   }
   ARN_MARK(1);
   // pass 1: h1 = V^H w
-  arn_dots(Vb, ldb, nc, ws, len, P1 + (int64_t)blockIdx.x * g.ldp);
+  arn_dots(Vb, ldb, nc, ws, len, P1);
   ARN_MARK(2);
   grid.sync();
   ARN_MARK(3);
   // every block's non-finite flag is set before the first barrier
   if (blockIdx.x == 0 && threadIdx.x == 32) gq.nonfinite = *((volatile int*)g.nonfinite);
-  arn_reduce(P1, g.ldp, nblk, nc, hsm);
+  arn_reduce(P1, nblk, nc, hsm);
   __syncthreads();
   if (blockIdx.x == 0)
     for (int c = threadIdx.x; c < nc; c += ARN_THREADS) {
@@ -377,14 +398,16 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
       sm[g.ldp + c] = hsm[c];
     }
   __syncthreads();
+  ARN_MARK(10);
   // pass 2: w -= V h1, h2 = V^H w
   arn_update(Vb, ldb, nc, hsm, ws, len);
   __syncthreads();
-  arn_dots(Vb, ldb, nc, ws, len, P2 + (int64_t)blockIdx.x * g.ldp);
+  ARN_MARK(11);
+  arn_dots(Vb, ldb, nc, ws, len, P2);
   ARN_MARK(4);
   grid.sync();
   ARN_MARK(5);
-  arn_reduce(P2, g.ldp, nblk, nc, hsm);
+  arn_reduce(P2, nblk, nc, hsm);
   __syncthreads();
   if (blockIdx.x == 0)
     for (int c = threadIdx.x; c < nc; c += ARN_THREADS) {
@@ -408,13 +431,13 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
     if (threadIdx.x == 0) {
       double2 s = make_double2(0.0, 0.0);
       for (int i = 0; i < ARN_THREADS / 32; ++i) s = cadd(s, red[i]);
-      st_cg(P1 + (int64_t)blockIdx.x * g.ldp, s);  // P1 is free: pass-1 partials consumed
+      st_cg(P1 + blockIdx.x, s);  // P1 is free: pass-1 partials consumed
     }
   }
   ARN_MARK(6);
   grid.sync();
   ARN_MARK(7);
-  arn_reduce(P1, g.ldp, nblk, 1, hsm);
+  arn_reduce(P1, nblk, 1, hsm);
   __syncthreads();
   const double hn = sqrt(hsm[0].x);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -435,10 +458,10 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
 #ifdef PT_ARN_PROFILE
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
     printf("ARN j=%d blk=%d stage %llu dots1 %llu sync1 %llu red+upd+dots2 %llu sync2 %llu "
-           "red+upd+norm %llu sync3 %llu red+givens %llu normalize %llu total %llu\n",
+           "red+upd+norm %llu sync3 %llu red+givens %llu normalize %llu total %llu [red1 %llu upd1 %llu]\n",
            j, blockIdx.x, tm[1] - tm[0], tm[2] - tm[1], tm[3] - tm[2], tm[4] - tm[3],
            tm[5] - tm[4], tm[6] - tm[5], tm[7] - tm[6], tm[8] - tm[7], tm[9] - tm[8],
-           tm[9] - tm[0]);
+           tm[9] - tm[0], tm[10] - tm[3], tm[11] - tm[10]);
 #endif
 }
 
