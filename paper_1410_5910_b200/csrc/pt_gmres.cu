@@ -17,6 +17,7 @@
 // once when the status says the solve has stopped: the host enqueues steps
 // ahead of its convergence check without changing the result.
 #ifdef PT_ARN_PROFILE
+#include <cstdlib>
 #include <cstdio>
 #endif
 #include <cooperative_groups.h>
@@ -113,11 +114,10 @@ __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.
 // the Arnoldi step while the reductions run: the one-thread rotation chain
 // then reads no global memory (a global load per rotation, ordered behind
 // the previous rotation's stores, cost ~0.4 us each: 14 us at j = 35).
+// Dynamic shared memory of the step: [coefficients | h1 | h2 | cs (.x) | sn]
+// (ldp complex values each; h1/h2 = CGS pass 1/2 coefficients of rows 0..j,
+// cs/sn = rotations 0..j-1), then the block's slice of w and of V.
 struct GivensSmem {
-  double2* h1;  // CGS pass-1 coefficients, rows 0..j
-  double2* h2;  // pass 2
-  double2* cs;  // rotation cosines in .x, rows 0..j-1
-  double2* sn;  // rotation sines
   double2 gj;   // g[j]
   double beta;
   double hist_w;  // hist[k - 1 - STAG_WINDOW] (k > STAG_WINDOW)
@@ -139,15 +139,22 @@ __device__ __noinline__ void givens_update(const GmresDev& g, const GivensSmem& 
   double2* Hj = g.Hraw + (int64_t)j * ldr;
   Hj[j + 1] = make_double2(hn, 0.0);
   // previous rotations down the new column; the running entry is carried in
-  // registers, the operands come from shared memory
-  double2 a = cadd(q.h1[0], q.h2[0]);
+  // registers, the operands come from shared memory (indexed off the
+  // dynamic shared-memory symbol, so the compiler knows they cannot alias
+  // the global stores and issues them ahead of the rotation chain)
+  extern __shared__ double2 gsm[];
+  const double2* h1 = gsm + g.ldp;
+  const double2* h2 = gsm + 2 * g.ldp;
+  const double2* cs = gsm + 3 * g.ldp;
+  const double2* sn = gsm + 4 * g.ldp;
+  double2 a = cadd(h1[0], h2[0]);
   Hj[0] = a;
 #pragma unroll 4
   for (int i = 0; i < j; ++i) {
-    const double2 b = cadd(q.h1[i + 1], q.h2[i + 1]);
+    const double2 b = cadd(h1[i + 1], h2[i + 1]);
     Hj[i + 1] = b;
-    const double c = q.cs[i].x;
-    const double2 s = q.sn[i];
+    const double c = cs[i].x;
+    const double2 s = sn[i];
     Rj[i] = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
     a = cadd(cmul(make_double2(-s.x, s.y), a), make_double2(c * b.x, c * b.y));
   }
@@ -311,13 +318,7 @@ k_arnoldi(GmresDev g, double rel_tol, int max_iter, cudaGraphConditionalHandle c
   const int64_t lo = (int64_t)blockIdx.x * chunk;
   const int len = (int)(lo + chunk < g.n ? chunk : (lo < g.n ? g.n - lo : 0));
   double2* hsm = sm;                  // coefficients (ldp)
-  __shared__ GivensSmem gq;           // block 0: the Givens update's operands
-  if (threadIdx.x == 0) {
-    gq.h1 = sm + g.ldp;
-    gq.h2 = sm + 2 * g.ldp;
-    gq.cs = sm + 3 * g.ldp;
-    gq.sn = sm + 4 * g.ldp;
-  }
+  __shared__ GivensSmem gq;           // block 0: the Givens update's scalar operands
   double2* ws = sm + ARN_SMEM_VECS * g.ldp;  // the block's slice of w
   double2* vs = ws + chunk;           // the block's slice of V[:, 0..j] (when it fits)
   double2* w = g.V + (int64_t)(j + 1) * g.n;
@@ -607,11 +608,20 @@ cudaError_t gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
   cfg.blockDim = dim3(ARN_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (g.l2_window > 0) {
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = g.V;
+    attr[1].val.accessPolicyWindow.num_bytes = g.l2_window;
+    attr[1].val.accessPolicyWindow.hitRatio = g.l2_hit;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, k_arnoldi, g, rel_tol, max_iter, cond);
 }
 
@@ -620,6 +630,31 @@ cudaError_t gm_arnoldi_setup(GmresDev& g, int device) {
   cudaError_t e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return e;
   g.arn_blocks = nsm < ARN_MAX_BLOCKS ? nsm : ARN_MAX_BLOCKS;
+  g.l2_window = 0;
+  g.l2_hit = 0.f;
+  {  // basis kept in L2 across iterations (PT_ARN_L2=1; off by default: at c3
+     // the staging phase gains ~0.7 us but the executor loses more, solve
+     // 18.32 -> 18.39 ms)
+    const char* env = std::getenv("PT_ARN_L2");
+    int persist = 0, window = 0;
+    if (env && env[0] == '1' &&
+        cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess &&
+        cudaDeviceGetAttribute(&window, cudaDevAttrMaxAccessPolicyWindowSize, device) == cudaSuccess &&
+        persist > 0 && window > 0) {
+      const size_t vbytes = (size_t)(g.max_iter + 1) * (size_t)g.n * sizeof(double2);
+      const size_t win = std::min(vbytes, (size_t)window);
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      const size_t want = std::min(win, (size_t)persist);
+      if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      if (cur > 0) {
+        g.l2_window = win;
+        g.l2_hit = (float)std::min(1.0, (double)cur / (double)win);
+      }
+    }
+    cudaGetLastError();
+  }
   const int64_t chunk = (g.n + g.arn_blocks - 1) / g.arn_blocks;
   int maxdyn = 0;
   e = cudaDeviceGetAttribute(&maxdyn, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
