@@ -462,8 +462,12 @@ def run_ours(args):
         "solve": {"per_iteration_ms": (total_ms / args.steps / len(mine)) / max(k, 1),
                   "solves_per_step": solves_per_step,
                   "solve_gbs": per_step_bytes / (total_ms / args.steps / len(mine) * 1e-3) / 1e9,
-                  "solve_frac": per_step_bytes / (total_ms / args.steps / len(mine) * 1e-3) / 1e9
-                  / peak,
+                  # solve-level fraction in the roofline's own unit: HBM bytes per
+                  # solve time, or (batched) the lockstep batch's flops per step time
+                  "solve_frac": ((exec_bytes / 16 * 8 * min(len(mine), 64)) / (total_ms * 1e-3) / 1e12
+                                 / peak if batched else
+                                 per_step_bytes / (total_ms / args.steps / len(mine) * 1e-3) / 1e9
+                                 / peak),
                   "algorithmic_bytes_per_solve": per_step_bytes,
                   "upload_s": upload_s, "offline_host_s": meta.get("offline_seconds")},
         "e2e": {"value": e2e_total / (args.steps * solves_per_step), "unit": "ms",
