@@ -78,19 +78,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-// Polling without acquire semantics: ld.acquire.gpu compiles to a strong
-// load plus an L1 invalidation (CCTL.IVALL) per load; a poll loop issues the
-// relaxed load and the waiter takes one acquire fence once every counter is
-// seen satisfied (fence_acquire_gpu below).
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_acquire_gpu() {
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
-
 __device__ __forceinline__ double2 warp_sum(double2 v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

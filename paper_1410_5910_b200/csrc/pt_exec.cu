@@ -70,11 +70,6 @@ __shared__ volatile uint32_t s_next_pos; // first unreserved ring position
 __shared__ volatile uint32_t s_consumed;
 __shared__ volatile unsigned s_seen[EXEC_TSLOTS];  // counters seen satisfied (staggered polling)
 constexpr int POLL_LANES = 8;
-#ifndef PT_POLL_RELAXED
-#define PT_POLL_RELAXED 1
-#endif
-constexpr bool POLL_RELAXED = PT_POLL_RELAXED != 0;
-#define POLL_LD(p) (POLL_RELAXED ? ld_relaxed(p) : ld_acquire(p))
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -413,7 +408,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
       const int nw = t.nwait;
       bool ok = true;
       for (int i = lane; i < nw; i += 32)
-        if (POLL_LD(a.ctr + w[i].ctr) < w[i].val) ok = false;
+        if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
       ok = __all_sync(0xffffffffu, ok);
       if (!ok && a.poll_stagger > 0 && nw * POLL_LANES <= 32) {
         // few counters: POLL_LANES lanes per counter, their polls staggered
@@ -429,7 +424,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
           }
           for (;;) {
             if ((s_seen[k] >> c) & 1u) break;
-            if (POLL_LD(a.ctr + w[c].ctr) >= w[c].val) {
+            if (ld_acquire(a.ctr + w[c].ctr) >= w[c].val) {
               atomicOr((unsigned*)&s_seen[k], 1u << c);
               break;
             }
@@ -441,13 +436,10 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
           if (a.poll_ns > 0) __nanosleep(a.poll_ns);
           ok = true;
           for (int i = lane; i < nw; i += 32)
-            if (POLL_LD(a.ctr + w[i].ctr) < w[i].val) ok = false;
+            if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
           ok = __all_sync(0xffffffffu, ok);
         }
       }
-      // every counter seen satisfied with relaxed polls: one acquire fence
-      // orders the producers' outputs before this task's reads
-      if (POLL_RELAXED) fence_acquire_gpu();
     }
     if (lane == 0) trace_mark(a, q, 1);
     __syncwarp();
