@@ -105,39 +105,71 @@ k_trsv(const int* __restrict__ order, int n, const int64_t* __restrict__ ptr,
 // separator is a contiguous run of rows whose diagonal block L_SS (U_SS) is
 // triangular and dense enough to invert once at create time.  A block's solve
 // is then two parallel steps: r = b_S - L_S,ext x_ext (the entries outside the
-// block, behind the global flags of earlier blocks), x_S = L_SS^-1 r (a dense
-// product) -- instead of one flag round trip per row of the block.  Blocks are
-// queued by their dependency level (the depth of the dissection tree).
+// block), x_S = L_SS^-1 r (a dense product) -- instead of one flag round trip
+// per row of the block.  Blocks are queued by their dependency level (the
+// depth of the dissection tree) and a block waits, once, for every block of
+// the lower levels: a done counter reaching qwait[q] (the number of blocks
+// queued before q's level).  Completions arrive level by level (a block
+// starts only after all lower levels are done), so the count is exact.  The
+// off-block product then issues all its loads at once, where a flag check
+// per entry cost two dependent L2 round trips per entry.
 constexpr int TRSV_BLOCK_MAX = 256;
-constexpr int TRSV_BLOCK_THREADS = 256;
+#ifndef PT_TRSV_THREADS
+#define PT_TRSV_THREADS 256
+#endif
+// threads per block solve (c3 Newton solve: 64 / 128 / 256 / 512 / 1024
+// threads 9.8 / 6.6 / 5.5-6.0 / 7.0 / 17.4 ms -- the many small blocks of the
+// lower levels want many resident CTAs)
+constexpr int TRSV_BLOCK_THREADS = PT_TRSV_THREADS;
 __global__ void __launch_bounds__(TRSV_BLOCK_THREADS)
-k_trsv_block(const int* __restrict__ border, const int* __restrict__ bstart,
-             const int* __restrict__ blen, const int64_t* __restrict__ boff,
-             const double2* __restrict__ binv, int nblocks, const int64_t* __restrict__ ptr,
-             const int* __restrict__ col, const double2* __restrict__ val, const double2* b,
-             double2* x, int* flag, int epoch, int* head, int spin_ns) {
+k_trsv_block(const int* __restrict__ border, const int* __restrict__ qwait,
+             const int* __restrict__ bstart, const int* __restrict__ blen,
+             const int64_t* __restrict__ boff, const double2* __restrict__ binv, int nblocks,
+             const int64_t* __restrict__ ptr, const int* __restrict__ col,
+             const double2* __restrict__ val, const double2* b, double2* x, int* head, int* done,
+             int spin_ns) {
   __shared__ double2 r[TRSV_BLOCK_MAX];
   __shared__ int s_q;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (;;) {
-    if (threadIdx.x == 0) s_q = atomicAdd(head, 1);
+    if (threadIdx.x == 0) {
+      const int q = atomicAdd(head, 1);
+      if (q < nblocks) {
+        const int need = __ldg(qwait + q);
+        while (ld_acquire(done) < need)
+          if (spin_ns) __nanosleep(spin_ns);
+      }
+      s_q = q;
+    }
     __syncthreads();
     const int q = s_q;
     if (q >= nblocks) return;
     const int blk = __ldg(border + q);
     const int s0 = __ldg(bstart + blk), len = __ldg(blen + blk);
-    // r = b_S - (entries outside the block) . x
+    // r = b_S - (entries outside the block) . x   (x of lower levels: final)
     for (int k = wid; k < len; k += nw) {
       const int i = s0 + k;
       const int64_t e0 = __ldg(ptr + i), e1 = __ldg(ptr + i + 1);
       double2 acc = make_double2(0.0, 0.0);
-      for (int64_t e = e0 + lane; e < e1; e += 32) {
-        const int j = __ldg(col + e);
-        if (j >= s0 && j < s0 + len) continue;  // inside the block: the inverse handles it
-        const double2 v = __ldg(val + e);
-        while (ld_acquire(flag + j) != epoch)
-          if (spin_ns) __nanosleep(spin_ns);
-        acc = cfma(v, ld_cg(x + j), acc);
+      // four entries per lane in flight (lane order kept: e, e + 32, ...);
+      // entries inside the block are left to the inverse
+      for (int64_t e = e0 + lane; e < e1; e += 128) {
+        int j[4];
+        double2 v[4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t f = e + 32 * u;
+          j[u] = f < e1 ? __ldg(col + f) : s0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool out = j[u] < s0 || j[u] >= s0 + len;
+          v[u] = out ? __ldg(val + e + 32 * u) : make_double2(0.0, 0.0);
+          xv[u] = out ? ld_cg(x + j[u]) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j[u] < s0 || j[u] >= s0 + len) acc = cfma(v[u], xv[u], acc);
       }
       acc = warp_sum(acc);
       if (lane == 0) r[k] = csub(ld_cg(b + i), acc);
@@ -149,12 +181,11 @@ k_trsv_block(const int* __restrict__ border, const int* __restrict__ bstart,
       double2 acc = make_double2(0.0, 0.0);
       for (int j = lane; j < len; j += 32) acc = cfma(__ldg(inv + (int64_t)k * len + j), r[j], acc);
       acc = warp_sum(acc);
-      if (lane == 0) {
-        st_cg(x + s0 + k, acc);
-        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag + s0 + k), "r"(epoch) : "memory");
-      }
+      if (lane == 0) st_cg(x + s0 + k, acc);
     }
-    __syncthreads();  // r is reused by the next block
+    __syncthreads();  // r is reused by the next block; x_S written
+    if (threadIdx.x == 0)  // release: the block's x_S before the count
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(done) : "memory");
   }
 }
 
@@ -275,7 +306,7 @@ struct pt_local {
   double2 *y = nullptr, *w = nullptr, *z = nullptr;
   double2* newton = nullptr;  // Newton traces scratch (n_layers x 4 x nxe)
   int* flag = nullptr;  // [rows] for L, [rows] for U
-  int* head = nullptr;  // queue heads (2 per solve)
+  int* head = nullptr;  // queue heads and block done counters (2 + 2 per solve)
   int epoch = 0;
   int grid = 0;
   int spin_ns = 0;  // back-off of a warp waiting on a dependency (PT_TRSV_SPIN)
@@ -286,6 +317,7 @@ struct pt_local {
   bool blocked = false;  // every layer passed its dissection blocks (PT_TRSV_BLOCK=0: off)
   int nblocks = 0;
   int *bstart = nullptr, *blen = nullptr, *l_border = nullptr, *u_border = nullptr;
+  int *l_qwait = nullptr, *u_qwait = nullptr;  // per queue index: blocks of lower levels
   int64_t *l_boff = nullptr, *u_boff = nullptr;
   double2 *l_binv = nullptr, *u_binv = nullptr;
   int bgrid = 0;
@@ -295,7 +327,8 @@ struct pt_local {
                     (void*)l_val, (void*)u_val, (void*)l_dinv, (void*)u_dinv, (void*)l_order,
                     (void*)u_order, (void*)q_in, (void*)q_out, (void*)y, (void*)w, (void*)z, (void*)newton,
                     (void*)flag, (void*)head, (void*)bstart, (void*)blen, (void*)l_border,
-                    (void*)u_border, (void*)l_boff, (void*)u_boff, (void*)l_binv, (void*)u_binv})
+                    (void*)u_border, (void*)l_qwait, (void*)u_qwait, (void*)l_boff, (void*)u_boff,
+                    (void*)l_binv, (void*)u_binv})
       cudaFree(p);
   }
 };
@@ -419,7 +452,8 @@ void invert_block(const std::vector<int64_t>& ptr, const std::vector<int>& col,
 // upper: on later ones), and the level count
 std::vector<int> block_queue(const std::vector<int64_t>& ptr, const std::vector<int>& col,
                              const std::vector<int>& bstart, const std::vector<int>& blen,
-                             const std::vector<int>& bid, bool lower, int32_t* nlev) {
+                             const std::vector<int>& bid, bool lower, int32_t* nlev,
+                             std::vector<int>& qwait) {
   const int nb = (int)bstart.size();
   std::vector<int> lev(nb, 0);
   for (int t = 0; t < nb; ++t) {
@@ -432,7 +466,14 @@ std::vector<int> block_queue(const std::vector<int64_t>& ptr, const std::vector<
       }
     lev[b2] = lv;
   }
-  return level_order(lev, nlev);
+  std::vector<int> order = level_order(lev, nlev);
+  // qwait[q]: blocks queued at lower levels than queue entry q's
+  std::vector<int> below(*nlev + 1, 0);
+  for (int v : lev) below[v + 1]++;
+  for (int v = 0; v < *nlev; ++v) below[v + 1] += below[v];
+  qwait.resize(nb);
+  for (int q = 0; q < nb; ++q) qwait[q] = below[lev[order[q]]];
+  return order;
 }
 
 int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) {
@@ -440,10 +481,10 @@ int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) 
   count_launch();
   if (h->blocked) {
     k_trsv_block<<<h->bgrid, TRSV_BLOCK_THREADS, 0, s>>>(
-        lower ? h->l_border : h->u_border, h->bstart, h->blen, lower ? h->l_boff : h->u_boff,
-        lower ? h->l_binv : h->u_binv, h->nblocks, lower ? h->l_ptr : h->u_ptr,
-        lower ? h->l_col : h->u_col, lower ? h->l_val : h->u_val, b, x,
-        h->flag + (lower ? 0 : h->rows), e, h->head + (lower ? 0 : 1), h->spin_ns);
+        lower ? h->l_border : h->u_border, lower ? h->l_qwait : h->u_qwait, h->bstart, h->blen,
+        lower ? h->l_boff : h->u_boff, lower ? h->l_binv : h->u_binv, h->nblocks,
+        lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col, lower ? h->l_val : h->u_val, b,
+        x, h->head + (lower ? 0 : 1), h->head + (lower ? 2 : 3), h->spin_ns);
     LCK(cudaGetLastError());
     return 0;
   }
@@ -459,7 +500,7 @@ int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) 
 // b -> z for every layer: L w = y (y gathered by the caller), U z = w
 int solve_all(pt_local* h, cudaStream_t s) {
   ++h->epoch;
-  LCK(cudaMemsetAsync(h->head, 0, 2 * sizeof(int), s));
+  LCK(cudaMemsetAsync(h->head, 0, 4 * sizeof(int), s));  // queue heads, done counters
   int rc;
   if ((rc = trsv(h, true, h->y, h->w, s))) return rc;
   return trsv(h, false, h->w, h->z, s);
@@ -545,7 +586,7 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   h->factor_nnz = (int64_t)lval.size() + (int64_t)uval.size() + 2 * row0;
   std::vector<int> lord = level_order(llev, &h->l_levels), uord = level_order(ulev, &h->u_levels);
   if (const char* e = std::getenv("PT_TRSV_BLOCK")) blocked = blocked && std::atoi(e) != 0;
-  std::vector<int> lbord, ubord;
+  std::vector<int> lbord, ubord, lqw, uqw;
   std::vector<int64_t> lboff, uboff;
   std::vector<double2> lbinv, ubinv;
   if (blocked) {
@@ -558,8 +599,8 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
       uboff.push_back((int64_t)ubinv.size());
       invert_block(uptr, ucol, uval, udinv, bstart[k], blen[k], false, ubinv);
     }
-    lbord = block_queue(lptr, lcol, bstart, blen, bid, true, &h->l_blevels);
-    ubord = block_queue(uptr, ucol, bstart, blen, bid, false, &h->u_blevels);
+    lbord = block_queue(lptr, lcol, bstart, blen, bid, true, &h->l_blevels, lqw);
+    ubord = block_queue(uptr, ucol, bstart, blen, bid, false, &h->u_blevels, uqw);
     h->nblocks = (int)bstart.size();
   }
   h->blocked = blocked;
@@ -572,7 +613,8 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
     return rc;
   if (blocked &&
       ((rc = up(&h->bstart, bstart)) || (rc = up(&h->blen, blen)) || (rc = up(&h->l_border, lbord)) ||
-       (rc = up(&h->u_border, ubord)) || (rc = up(&h->l_boff, lboff)) || (rc = up(&h->u_boff, uboff)) ||
+       (rc = up(&h->u_border, ubord)) || (rc = up(&h->l_qwait, lqw)) || (rc = up(&h->u_qwait, uqw)) ||
+       (rc = up(&h->l_boff, lboff)) || (rc = up(&h->u_boff, uboff)) ||
        (rc = up(&h->l_binv, lbinv)) || (rc = up(&h->u_binv, ubinv))))
     return rc;
   LCK(cudaMalloc(&h->y, row0 * sizeof(double2)));
@@ -580,7 +622,7 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   LCK(cudaMalloc(&h->z, row0 * sizeof(double2)));
   LCK(cudaMalloc(&h->flag, 2 * row0 * sizeof(int)));
   LCK(cudaMemset(h->flag, 0, 2 * row0 * sizeof(int)));
-  LCK(cudaMalloc(&h->head, 2 * sizeof(int)));
+  LCK(cudaMalloc(&h->head, 4 * sizeof(int)));
   int nsm = 0, occ = 0;
   LCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv, 1024, 0));
