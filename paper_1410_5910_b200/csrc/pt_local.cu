@@ -189,6 +189,83 @@ k_trsv_block(const int* __restrict__ border, const int* __restrict__ qwait,
   }
 }
 
+// Lower levels (every block of the level at most 32 rows: the dissection
+// leaves and short separators, ~all of the blocks): one WARP per block, lane k
+// owns row k.  Warps grab chunks of TRSV_WARP_CHUNK consecutive queue entries
+// (level order) from a queue head, so a block waited on was always grabbed by
+// a running warp (no residency assumption), and count their solved blocks
+// per level into the level's done counter, flushing before any wait.  A block
+// of level l waits for level l - 1's counter to be complete (levels complete
+// in order).  Per block: r_k = b_k - (off-block entries of row k) . x, then
+// x_k = sum_j inv[k, j] r_j with r_j broadcast by shuffles.
+constexpr int TRSV_WARP_MAX = 32;
+constexpr int TRSV_WARP_CHUNK = 8;
+__global__ void __launch_bounds__(256)
+k_trsv_warp(const int* __restrict__ border, const int* __restrict__ qlev,
+            const int* __restrict__ lq0, int nq, const int* __restrict__ bstart,
+            const int* __restrict__ blen, const int64_t* __restrict__ boff,
+            const double2* __restrict__ binv, const int64_t* __restrict__ ptr,
+            const int* __restrict__ col, const double2* __restrict__ val, const double2* b,
+            double2* x, int* lvl_done, int* whead, int spin_ns) {
+  const int lane = threadIdx.x & 31;
+  int known = 0;     // levels below this one are known complete
+  int pend_l = -1;   // level of the solved blocks not yet counted
+  int pend_n = 0;
+  auto flush = [&]() {
+    __syncwarp();  // every lane's x stores before the release
+    if (lane == 0 && pend_n > 0)
+      asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(lvl_done + pend_l), "r"(pend_n)
+                   : "memory");
+    pend_n = 0;
+  };
+  for (;;) {
+    int q0 = 0;
+    if (lane == 0) q0 = atomicAdd(whead, TRSV_WARP_CHUNK);
+    q0 = __shfl_sync(0xffffffffu, q0, 0);
+    if (q0 >= nq) break;
+    const int q1 = min(q0 + TRSV_WARP_CHUNK, nq);
+    for (int q = q0; q < q1; ++q) {
+      const int l = __ldg(qlev + q);
+      if (l != pend_l) {
+        flush();
+        pend_l = l;
+      }
+      if (l > known) {  // wait for level l - 1 (and so every lower level)
+        flush();
+        const int need = __ldg(lq0 + l) - __ldg(lq0 + l - 1);
+        if (lane == 0)
+          while (ld_acquire(lvl_done + l - 1) < need)
+            if (spin_ns) __nanosleep(spin_ns);
+        __syncwarp();
+        known = l;
+      }
+      const int blk = __ldg(border + q);
+      const int s0 = __ldg(bstart + blk), len = __ldg(blen + blk);
+      double2 r = make_double2(0.0, 0.0);
+      if (lane < len) {
+        const int i = s0 + lane;
+        const int64_t e0 = __ldg(ptr + i), e1 = __ldg(ptr + i + 1);
+        double2 acc = make_double2(0.0, 0.0);
+        for (int64_t e = e0; e < e1; ++e) {
+          const int j = __ldg(col + e);
+          if (j < s0 || j >= s0 + len) acc = cfma(__ldg(val + e), ld_cg(x + j), acc);
+        }
+        r = csub(ld_cg(b + i), acc);
+      }
+      const double2* inv = binv + __ldg(boff + blk) + (int64_t)lane * len;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int jj = 0; jj < len; ++jj) {
+        const double2 rj = make_double2(__shfl_sync(0xffffffffu, r.x, jj),
+                                        __shfl_sync(0xffffffffu, r.y, jj));
+        if (lane < len) acc = cfma(__ldg(inv + jj), rj, acc);
+      }
+      if (lane < len) st_cg(x + s0 + lane, acc);
+      ++pend_n;
+    }
+  }
+  flush();
+}
+
 // y[G] = b_layer[q_in[k]] for every global row G = row0 + k.  b_layer is the
 // layer's forcing in natural (z, x) order: f restricted to the layer rows
 // (restrict_source, partition.py:104-113) plus, when x_traces is given, the
@@ -318,6 +395,11 @@ struct pt_local {
   int nblocks = 0;
   int *bstart = nullptr, *blen = nullptr, *l_border = nullptr, *u_border = nullptr;
   int *l_qwait = nullptr, *u_qwait = nullptr;  // per queue index: blocks of lower levels
+  // warp-per-block prefix of each queue (levels whose blocks all have <= 32
+  // rows): level starts lq0[0..nlev], queue split
+  int *l_lq0 = nullptr, *u_lq0 = nullptr, *l_qlev = nullptr, *u_qlev = nullptr;
+  int l_wlev = 0, u_wlev = 0, l_split = 0, u_split = 0;
+  int wgrid = 0;
   int64_t *l_boff = nullptr, *u_boff = nullptr;
   double2 *l_binv = nullptr, *u_binv = nullptr;
   int bgrid = 0;
@@ -327,7 +409,8 @@ struct pt_local {
                     (void*)l_val, (void*)u_val, (void*)l_dinv, (void*)u_dinv, (void*)l_order,
                     (void*)u_order, (void*)q_in, (void*)q_out, (void*)y, (void*)w, (void*)z, (void*)newton,
                     (void*)flag, (void*)head, (void*)bstart, (void*)blen, (void*)l_border,
-                    (void*)u_border, (void*)l_qwait, (void*)u_qwait, (void*)l_boff, (void*)u_boff,
+                    (void*)u_border, (void*)l_qwait, (void*)u_qwait, (void*)l_lq0, (void*)u_lq0, (void*)l_qlev, (void*)u_qlev,
+                    (void*)l_boff, (void*)u_boff,
                     (void*)l_binv, (void*)u_binv})
       cudaFree(p);
   }
@@ -478,16 +561,30 @@ std::vector<int> block_queue(const std::vector<int64_t>& ptr, const std::vector<
 
 int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) {
   const int e = h->epoch;
-  count_launch();
   if (h->blocked) {
-    k_trsv_block<<<h->bgrid, TRSV_BLOCK_THREADS, 0, s>>>(
-        lower ? h->l_border : h->u_border, lower ? h->l_qwait : h->u_qwait, h->bstart, h->blen,
-        lower ? h->l_boff : h->u_boff, lower ? h->l_binv : h->u_binv, h->nblocks,
-        lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col, lower ? h->l_val : h->u_val, b,
-        x, h->head + (lower ? 0 : 1), h->head + (lower ? 2 : 3), h->spin_ns);
-    LCK(cudaGetLastError());
+    const int split = lower ? h->l_split : h->u_split;
+    const int* border = lower ? h->l_border : h->u_border;
+    if (split > 0) {  // small lower levels: a warp per block
+      k_trsv_warp<<<h->wgrid, 256, 0, s>>>(
+          border, lower ? h->l_qlev : h->u_qlev, lower ? h->l_lq0 : h->u_lq0, split, h->bstart,
+          h->blen, lower ? h->l_boff : h->u_boff, lower ? h->l_binv : h->u_binv,
+          lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col, lower ? h->l_val : h->u_val, b,
+          x, h->head + (lower ? 4 : 4 + 32), h->head + (lower ? 68 : 69), h->spin_ns);
+      LCK(cudaGetLastError());
+      count_launch();
+    }
+    if (split < h->nblocks) {
+      count_launch();  // the rest: a CTA per block (qwait counts past the split)
+      k_trsv_block<<<h->bgrid, TRSV_BLOCK_THREADS, 0, s>>>(
+          border + split, (lower ? h->l_qwait : h->u_qwait) + split, h->bstart, h->blen,
+          lower ? h->l_boff : h->u_boff, lower ? h->l_binv : h->u_binv, h->nblocks - split,
+          lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col, lower ? h->l_val : h->u_val, b,
+          x, h->head + (lower ? 0 : 1), h->head + (lower ? 2 : 3), h->spin_ns);
+      LCK(cudaGetLastError());
+    }
     return 0;
   }
+  count_launch();
   k_trsv<<<h->grid, 1024, 0, s>>>(lower ? h->l_order : h->u_order, (int)h->rows,
                                   lower ? h->l_ptr : h->u_ptr, lower ? h->l_col : h->u_col,
                                   lower ? h->l_val : h->u_val, lower ? h->l_dinv : h->u_dinv, b, x,
@@ -500,7 +597,9 @@ int trsv(pt_local* h, bool lower, const double2* b, double2* x, cudaStream_t s) 
 // b -> z for every layer: L w = y (y gathered by the caller), U z = w
 int solve_all(pt_local* h, cudaStream_t s) {
   ++h->epoch;
-  LCK(cudaMemsetAsync(h->head, 0, 4 * sizeof(int), s));  // queue heads, done counters
+  // queue heads, done counters, per-level done counters and queue heads of
+  // the warp prefix
+  LCK(cudaMemsetAsync(h->head, 0, (4 + 64 + 2) * sizeof(int), s));
   int rc;
   if ((rc = trsv(h, true, h->y, h->w, s))) return rc;
   return trsv(h, false, h->w, h->z, s);
@@ -586,7 +685,7 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   h->factor_nnz = (int64_t)lval.size() + (int64_t)uval.size() + 2 * row0;
   std::vector<int> lord = level_order(llev, &h->l_levels), uord = level_order(ulev, &h->u_levels);
   if (const char* e = std::getenv("PT_TRSV_BLOCK")) blocked = blocked && std::atoi(e) != 0;
-  std::vector<int> lbord, ubord, lqw, uqw;
+  std::vector<int> lbord, ubord, lqw, uqw, llq0, ulq0, lqlev, uqlev;
   std::vector<int64_t> lboff, uboff;
   std::vector<double2> lbinv, ubinv;
   if (blocked) {
@@ -601,6 +700,34 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
     }
     lbord = block_queue(lptr, lcol, bstart, blen, bid, true, &h->l_blevels, lqw);
     ubord = block_queue(uptr, ucol, bstart, blen, bid, false, &h->u_blevels, uqw);
+    // warp prefix: the leading levels whose blocks all have <= 32 rows (at
+    // most 32 levels); the CTA kernel's waits then count past the split
+    auto warp_prefix = [&](const std::vector<int>& bord, std::vector<int>& qw, std::vector<int>& lq0,
+                           std::vector<int>& qlev, int* wlev, int* split) {
+      lq0.assign(1, 0);
+      int q = 0;
+      const int nb = (int)bord.size();
+      // opt-in (PT_TRSV_WARP=1): measured slower at c3 (Newton 7.7 vs 5.5 ms),
+      // the large separator blocks of the upper levels dominate
+      const bool on = std::getenv("PT_TRSV_WARP") && std::atoi(std::getenv("PT_TRSV_WARP")) == 1;
+      while (on && q < nb && (int)lq0.size() <= 32) {
+        int e = q;
+        bool small = true;
+        for (; e < nb && qw[e] == qw[q]; ++e)
+          if (blen[bord[e]] > TRSV_WARP_MAX) small = false;
+        if (!small) break;
+        q = e;
+        lq0.push_back(q);
+      }
+      *wlev = (int)lq0.size() - 1;
+      *split = q;
+      qlev.assign(std::max(q, 1), 0);
+      for (int l = 0; l < *wlev; ++l)
+        for (int i = lq0[l]; i < lq0[l + 1]; ++i) qlev[i] = l;
+      for (int i = q; i < nb; ++i) qw[i] -= q;
+    };
+    warp_prefix(lbord, lqw, llq0, lqlev, &h->l_wlev, &h->l_split);
+    warp_prefix(ubord, uqw, ulq0, uqlev, &h->u_wlev, &h->u_split);
     h->nblocks = (int)bstart.size();
   }
   h->blocked = blocked;
@@ -614,6 +741,8 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   if (blocked &&
       ((rc = up(&h->bstart, bstart)) || (rc = up(&h->blen, blen)) || (rc = up(&h->l_border, lbord)) ||
        (rc = up(&h->u_border, ubord)) || (rc = up(&h->l_qwait, lqw)) || (rc = up(&h->u_qwait, uqw)) ||
+       (rc = up(&h->l_lq0, llq0)) || (rc = up(&h->u_lq0, ulq0)) ||
+       (rc = up(&h->l_qlev, lqlev)) || (rc = up(&h->u_qlev, uqlev)) ||
        (rc = up(&h->l_boff, lboff)) || (rc = up(&h->u_boff, uboff)) ||
        (rc = up(&h->l_binv, lbinv)) || (rc = up(&h->u_binv, ubinv))))
     return rc;
@@ -622,7 +751,7 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   LCK(cudaMalloc(&h->z, row0 * sizeof(double2)));
   LCK(cudaMalloc(&h->flag, 2 * row0 * sizeof(int)));
   LCK(cudaMemset(h->flag, 0, 2 * row0 * sizeof(int)));
-  LCK(cudaMalloc(&h->head, 4 * sizeof(int)));
+  LCK(cudaMalloc(&h->head, (4 + 64 + 2) * sizeof(int)));
   int nsm = 0, occ = 0;
   LCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv, 1024, 0));
@@ -634,6 +763,9 @@ int pt_local_create(const pt_local_layer* layers, int32_t n_layers, int device, 
   int bocc = 0;
   LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, k_trsv_block, TRSV_BLOCK_THREADS, 0));
   h->bgrid = nsm * std::max(bocc, 1);  // all resident: a waiting block never blocks its producers
+  int wocc = 0;
+  LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wocc, k_trsv_warp, 256, 0));
+  h->wgrid = nsm * std::max(wocc, 1);
   cudaSetDevice(prev);
   *out = h.release();
   return 0;
