@@ -97,3 +97,26 @@ def test_block_and_row_solves_agree(cuda_ok, monkeypatch):
     assert rel(loc.solve(b), rows.solve(b)) <= 1e-12
     assert rows.info["l_levels"] > loc.info["l_levels"]  # row levels vs block levels
     rows.close()
+
+
+@pytest.mark.parametrize("case", ["fx_plr", "c1"])
+def test_warp_prefix_solve_agrees(cuda_ok, monkeypatch, case):
+    """The optional warp-per-block path for the small lower levels
+    (PT_TRSV_WARP=1) gives the same layer solutions as the CTA-per-block
+    solve (c1 has levels with blocks above 32 rows: the prefix ends there
+    and the CTA kernel takes the rest)."""
+    from paper_1410_5910_b200.local import DeviceLocalSolver
+    if case.startswith("fx_"):
+        facs, geo, loc = local(case)
+        make = lambda: DeviceLocalSolver(facs, geo)  # noqa: E731
+    else:
+        loc = DeviceLocalSolver.from_config(case)
+        make = lambda: DeviceLocalSolver.from_config(case)  # noqa: E731
+    monkeypatch.setenv("PT_TRSV_WARP", "1")
+    warp = make()
+    rng = np.random.default_rng(9)
+    b = rng.standard_normal(loc.info["rows"]) + 1j * rng.standard_normal(loc.info["rows"])
+    assert rel(loc.solve(b), warp.solve(b)) <= 1e-12
+    warp.close()
+    if not case.startswith("fx_"):
+        loc.close()
