@@ -7,27 +7,28 @@
 // their own group's counter.  The launch is cooperative: every CTA is
 // resident, so a waiting task always has a running producer.
 //
-// Each CTA is warp-specialised.  Two producer warps own one task slot each
-// and take the CTA's tasks alternately (grabbed one at a time, in order);
-// per task a producer warp:
+// Each CTA is warp-specialised.  Three producer warps (EXEC_PRODUCERS) own
+// one task slot each and take the CTA's tasks in rotation (grabbed one at a
+// time, in order); per task a producer warp:
 //   - bulk-copies the task's metadata blob (descriptor, operator pieces,
 //     terms, eyes, waits, per-column items) into its slot: one TMA copy;
 //   - issues the task's operator pieces into the CTA's smem ring with TMA
 //     bulk copies (cp.async.bulk, mbarrier complete_tx) as far as the ring
 //     allows -- BEFORE the dependency wait, when it is this task's turn;
 //   - waits for the dependency counters;
-//   - gathers the vector inputs (source slice, t values, term sources,
-//     epilogue rows) with cp.async, all copies in flight at once;
+//   - stages the vector inputs (source slice, t values, term sources,
+//     epilogue rows) with TMA bulk copies, all in flight at once;
 //   - hands the slot to the consumers (mbarrier), then streams the task's
 //     remaining pieces and passes the ring to the next task.
-// With two producer warps the metadata, dependency and staging latency of
-// task n+1 overlaps the consumers' work on task n, and the operator stream
-// of the next sweep level overlaps the current level's dependency chain.
-// The 8 consumer warps compute from shared memory (FP64 FMA, fixed-order
-// sums), release ring stages and slots through mbarriers, write the outputs
-// and signal the counters.  No float atomics anywhere: every output element
-// is produced by one CTA in a fixed order, so repeated applies are bitwise
-// identical.
+// With three producer warps the metadata, dependency and staging latency of
+// tasks n+1 and n+2 overlaps the consumers' work on task n, and the operator
+// stream of the next sweep level overlaps the current level's dependency
+// chain.  The 16 consumer warps compute from shared memory (FP64 FMA,
+// fixed-order sums), release ring stages and slots through mbarriers and
+// write the outputs; the slot's producer warp then signals the counter
+// (red.release.gpu).  No float atomics anywhere: every output element is
+// produced by one CTA in a fixed order, so repeated applies are bitwise
+// identical.  The last CTA out resets the counters for the next launch.
 #include "pt_device.cuh"
 
 namespace pt {
