@@ -283,3 +283,25 @@ def test_c5_batch_parity(cuda_ok):
         x, rep = op.gmres(arr["rhs"][s], rel_tol=meta["gmres_tol"])
         assert abs(rep["iterations"] - meta["solves"][i]["iterations"]) <= 1
         assert rel(x[: nt * m] + x[nt * m:], arr["ref_traces"][i]) <= TRACE_TOL
+
+
+@pytest.mark.parametrize("name", FIXTURES[:2])
+def test_timed_solve_counts_only_launches_that_ran(cuda_ok, name):
+    """Per-launch timing (the bench's roofline pass) counts the executor
+    launches of one solve exactly: the M prologue, one fused A->M launch per
+    iteration and the A epilogue, with their programs' algorithmic bytes -- no
+    launch after the stop (they would add bytes at ~zero time).  The timed
+    solve equals the graph solve bitwise."""
+    meta, arr, op = get(name)
+    x_graph, r_graph = op.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"])
+    op.exec_timing(True)
+    try:
+        x, rep = op.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"])
+        ms, n, nbytes = op.exec_stats()
+    finally:
+        op.exec_timing(False)
+    k = rep["iterations"]
+    assert n == k + 2
+    assert nbytes == op.bytes_apply_M(2) + k * (op.bytes_apply_A() + op.bytes_apply_M(2)) + op.bytes_apply_A()
+    assert ms > 0.0
+    assert np.array_equal(x, x_graph) and rep["iterations"] == r_graph["iterations"]
