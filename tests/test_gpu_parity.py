@@ -305,3 +305,21 @@ def test_timed_solve_counts_only_launches_that_ran(cuda_ok, name):
     assert nbytes == op.bytes_apply_M(2) + k * (op.bytes_apply_A() + op.bytes_apply_M(2)) + op.bytes_apply_A()
     assert ms > 0.0
     assert np.array_equal(x, x_graph) and rep["iterations"] == r_graph["iterations"]
+
+
+@pytest.mark.parametrize("name", ["fx_plr", "fx_uneven"])
+def test_split_chain_queue_bitwise_equal(cuda_ok, monkeypatch, name):
+    """Scheduling does not change results: with the sweep-chain tasks on CTAs
+    of their own (PT_CHAIN_CTAS, a second queue) the preconditioner apply and
+    the fused iteration are bitwise equal to the single-queue executor's."""
+    meta, arr, op = get(name)
+    path = golden_path(name)
+    monkeypatch.setenv("PT_CHAIN_CTAS", "16")
+    m2, a2 = load_case_arrays(path)
+    op2 = DeviceOperator.from_arrays(m2, a2)
+    try:
+        x = np.asarray(arr["probe_x"]) if "probe_x" in arr else np.asarray(arr["rhs"][0])
+        assert np.array_equal(op.apply_M(x, n_it=2), op2.apply_M(x, n_it=2))
+        assert np.array_equal(op.apply_AM(x, n_it=2), op2.apply_AM(x, n_it=2))
+    finally:
+        op2.close()
