@@ -103,3 +103,18 @@ def test_large_case_plans(name):
     a, m2 = op.plan_stats("A"), op.plan_stats("M", 2)
     assert st["staged_bytes"] == a["staged_bytes"] + m2["staged_bytes"]
     assert st["staged_bytes"] <= a["algo_bytes"] + m2["algo_bytes"]
+
+
+@pytest.mark.parametrize("stages", [2, 3])
+@pytest.mark.parametrize("name", ["fx_plr", "c3r"])
+def test_task_pieces_fit_the_ring_window(name, stages, monkeypatch):
+    """A task never holds more pieces than the ring's parity window (2 stages
+    per ring stage): the producer would wait on its own unfinished task.
+    PT_T_PIECES above the window is clamped at pt_create, not planned."""
+    monkeypatch.setenv("PT_STAGES", str(stages))
+    monkeypatch.setenv("PT_T_PIECES", "16")
+    monkeypatch.setenv("PT_T_PIECES_CHAIN", "16")
+    op = host_op(name)
+    for kind, n_it in (("A", 0), ("M", 2), ("AM", 2)):
+        st = op.plan_stats(kind, n_it) if n_it else op.plan_stats(kind)
+        assert 1 <= st["max_pieces"] <= 2 * stages
