@@ -496,7 +496,7 @@ int check_slots(const pt_handle* h, const Program& pg) {
     if (t.type == TASK_Y_DENSE) vec = 2 * (int64_t)t.nterm * h->op.m;
     const int rows = t.type == TASK_Y_DENSE ? DENSE_RT_MAX : EXEC_EPI;
     if (vec > h->src_cap || t.nitem > h->item_cap || t.nterm > EXEC_TERMS ||
-        t.neye > EXEC_EYES || t.npiece > EXEC_PIECES || t.npiece > 2 * h->n_stages ||
+        t.neye > EXEC_EYES || t.npiece > EXEC_PIECES ||
         t.nwait > EXEC_WAITS ||
         t.nrun > h->run_cap || t.nsrun > h->srun_cap ||
         (t.type != TASK_T_PLR && t.r1 - t.r0 > rows))
@@ -960,10 +960,6 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_CTA_GBS")) h->pp.cta_gbs = std::atof(e);
   if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
     h->pp.t_pieces_chain = std::max(1, std::atoi(e));
-  // a task's pieces must fit the ring's parity window (s_consumed advances
-  // only when a task ends, pt_exec.cu): more than 2 * n_stages never issue
-  h->pp.t_pieces = std::min(h->pp.t_pieces, 2 * h->n_stages);
-  h->pp.t_pieces_chain = std::min(h->pp.t_pieces_chain, 2 * h->n_stages);
   if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
   *out = h.release();
   return 0;

@@ -63,11 +63,11 @@ __shared__ volatile int s_resv_turn;     // slot use that reserves positions nex
 __shared__ volatile uint32_t s_next_pos; // first unreserved ring position
 // Ring positions fully consumed (a lower bound: updated by the consumers at
 // the end of every task).  A stage's empty barrier is tested by parity, which
-// only tells apart two consecutive phases; a producer therefore looks at
-// position pos only while pos < s_consumed + 2 * n_stages (then the phase of
-// pos - n_stages is the current or the previous one).  Without the bound a
-// producer several uses ahead (long tasks, or more than two task slots) could
-// read an older phase as complete.
+// only tells apart two consecutive phases; a producer therefore looks at the
+// first positions of its use only while pos < s_consumed + 2 * n_stages (then
+// the phase of pos - n_stages is the current or the previous one), see
+// in_window.  Without the bound a producer several uses ahead (long tasks, or
+// more than two task slots) could read an older phase as complete.
 __shared__ volatile uint32_t s_consumed;
 __shared__ volatile unsigned s_seen[EXEC_TSLOTS];  // counters seen satisfied (staggered polling)
 constexpr int POLL_LANES = 8;
@@ -226,12 +226,22 @@ __device__ __forceinline__ void issue_piece(const ExecArgs& a, const Layout& L, 
   if (p < 8) trace_mark(a, q, 14 + p);
 }
 
+// The parity test of position pos (waiting for the consumption of pos - ns)
+// is valid once pos - ns has been issued: its issuer waited for pos - 2 ns.
+// A use issues its own positions in order, so only the first ns positions
+// of a use (pos - ns issued by an earlier use, perhaps not yet) need the
+// window bound pos < s_consumed + 2 ns; later ones never wait on their own
+// task's consumption (a task may hold any number of pieces).
+__device__ __forceinline__ bool in_window(uint32_t pos, uint32_t pos0, uint32_t ns) {
+  return pos >= pos0 + ns || pos < s_consumed + 2 * ns;
+}
+
 // lane 0: is the stage of ring position pos free (its previous occupant,
 // position pos - n_stages, consumed)?
-__device__ __forceinline__ bool stage_free(const Layout& L, uint32_t pos) {
+__device__ __forceinline__ bool stage_free(const Layout& L, uint32_t pos, uint32_t pos0) {
   const uint32_t ns = (uint32_t)L.n_stages;
   if (pos < ns) return true;
-  if (pos >= s_consumed + 2 * ns) return false;  // outside the parity window
+  if (!in_window(pos, pos0, ns)) return false;
   return bar_test(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
 }
 
@@ -399,7 +409,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
       __threadfence_block();
       s_resv_turn = use + 1;
       // pieces before the dependency wait, into stages already free
-      while (issued < t.npiece && stage_free(L, pos0 + issued)) {
+      while (issued < t.npiece && stage_free(L, pos0 + issued, pos0)) {
         issue_piece(a, L, sl, q, issued, pos0 + issued);
         ++issued;
       }
@@ -453,7 +463,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
       for (; issued < t.npiece; ++issued) {
         const uint32_t pos = pos0 + issued;
         if (pos >= ns) {
-          while (pos >= s_consumed + 2 * ns) __nanosleep(32);
+          while (!in_window(pos, pos0, ns)) __nanosleep(32);
           bar_wait(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
         }
         issue_piece(a, L, sl, q, issued, pos);

@@ -16,6 +16,7 @@ import ctypes as C
 import numpy as np
 
 from . import _native as nat
+from .operator import _writable
 
 __all__ = ["DeviceLocalSolver"]
 
@@ -105,7 +106,7 @@ class DeviceLocalSolver:
         a = np.asarray(a, dtype=np.complex128)
         if a.shape != shape:
             raise ValueError(f"{name} has shape {a.shape}, expected {shape}")
-        return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}"), True
+        return torch.from_numpy(_writable(a)).to(f"cuda:{self.device}"), True
 
     def solve(self, b):
         """x_l = H_l^-1 b_l for every layer (layers concatenated, natural order)."""

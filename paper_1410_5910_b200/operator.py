@@ -40,6 +40,13 @@ def _torch():
     return torch
 
 
+def _writable(a):
+    """A contiguous array torch.from_numpy can wrap without a warning: read-only
+    inputs (memory-mapped case files) are copied first."""
+    a = np.ascontiguousarray(a)
+    return a if a.flags.writeable else a.copy()
+
+
 def load_case_arrays(path):
     """(meta, arrays) of a PTC1 case; resolves ``operator_case`` links."""
     path = Path(path)
@@ -177,7 +184,7 @@ class DeviceOperator:
         if a.shape != (self.N,):
             raise ValueError(f"polarized vector has length {a.shape[0] if a.ndim else a.shape}, "
                              f"expected {self.N}")
-        return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}"), True
+        return torch.from_numpy(_writable(a)).to(f"cuda:{self.device}"), True
 
     def _out(self, out, host):
         torch = _torch()
@@ -260,7 +267,7 @@ class DeviceOperator:
         a = np.asarray(X, dtype=np.complex128)
         if a.ndim != 2 or a.shape[1] != self.N:
             raise ValueError(f"{name} must have shape (nrhs, {self.N}), got {a.shape}")
-        return torch.from_numpy(np.ascontiguousarray(a)).to(f"cuda:{self.device}"), True
+        return torch.from_numpy(_writable(a)).to(f"cuda:{self.device}"), True
 
     def apply_A_batch(self, X):
         """Y[s] = pol @ X[s] for every source row s (dense operators)."""

@@ -418,7 +418,7 @@ def _solve_helmholtz_device(state, f, precond, gmres, report, oracle):
     for k in ("iterations", "residual_history", "converged", "flag", "true_residual"):
         setattr(report, k, getattr(inner, k))
     report.traces = inner.traces
-    x_dev = x if hasattr(x, "data_ptr") else torch.from_numpy(np.asarray(x)).to(f_dev.device)
+    x_dev = x if hasattr(x, "data_ptr") else torch.from_numpy(np.array(x, dtype=np.complex128)).to(f_dev.device)
     u = stage("reconstruct", lambda: loc.reconstruct(f_dev, x_dev))
     report.u = u.cpu().numpy()
     n_c = loc.geo["n_c"]

@@ -78,7 +78,7 @@ def test_applies_bitwise_repeatable_and_linear(cuda_ok, name):
 
 def _fused_matches_separate(op, x):
     import torch
-    xd = torch.from_numpy(np.asarray(x)).cuda()
+    xd = torch.from_numpy(np.array(x)).cuda()
     ref = op.apply_M(op.apply_A(xd))
     for _ in range(8):  # a scheduling race would show up as a mismatch
         assert torch.equal(op.apply_AM(xd), ref)
@@ -307,18 +307,28 @@ def test_timed_solve_counts_only_launches_that_ran(cuda_ok, name):
     assert np.array_equal(x, x_graph) and rep["iterations"] == r_graph["iterations"]
 
 
-@pytest.mark.parametrize("name", ["fx_plr", "fx_uneven"])
-def test_split_chain_queue_bitwise_equal(cuda_ok, monkeypatch, name):
-    """Scheduling does not change results: with the sweep-chain tasks on CTAs
-    of their own (PT_CHAIN_CTAS, a second queue) the preconditioner apply and
-    the fused iteration are bitwise equal to the single-queue executor's."""
+VARIANTS = {
+    # long tasks: more pieces than the ring's parity window (2 x stages)
+    "long_tasks": {"PT_STAGES": "2", "PT_T_PIECES": "16", "PT_T_PIECES_CHAIN": "16"},
+    "two_stages": {"PT_STAGES": "2"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("name", ["fx_plr", "fx_uneven", "fx_extrap_plr", "fx_extrap"])
+def test_scheduling_variants_bitwise_equal(cuda_ok, monkeypatch, name, variant):
+    """Scheduling does not change results: with a different ring (two stages)
+    and tasks longer than the ring's parity window, the preconditioner apply
+    and the fused iteration are bitwise equal to the default executor's."""
     meta, arr, op = get(name)
     path = golden_path(name)
-    monkeypatch.setenv("PT_CHAIN_CTAS", "16")
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     m2, a2 = load_case_arrays(path)
     op2 = DeviceOperator.from_arrays(m2, a2)
     try:
         x = np.asarray(arr["probe_x"]) if "probe_x" in arr else np.asarray(arr["rhs"][0])
+        assert np.array_equal(op.apply_A(x), op2.apply_A(x))
         assert np.array_equal(op.apply_M(x, n_it=2), op2.apply_M(x, n_it=2))
         assert np.array_equal(op.apply_AM(x, n_it=2), op2.apply_AM(x, n_it=2))
     finally:

@@ -106,15 +106,17 @@ def test_large_case_plans(name):
 
 
 @pytest.mark.parametrize("stages", [2, 3])
-@pytest.mark.parametrize("name", ["fx_plr", "c3r"])
-def test_task_pieces_fit_the_ring_window(name, stages, monkeypatch):
-    """A task never holds more pieces than the ring's parity window (2 stages
-    per ring stage): the producer would wait on its own unfinished task.
-    PT_T_PIECES above the window is clamped at pt_create, not planned."""
+@pytest.mark.parametrize("name", ["fx_plr", "fx_extrap_plr", "fx_extrap", "c3r", "c4"])
+def test_long_tasks_plan_beyond_the_ring_window(name, stages, monkeypatch):
+    """A task may hold more pieces than the ring's parity window (2 x stages):
+    the producer applies the window bound only to a use's first n_stages
+    positions, so long tasks (PT_T_PIECES above the window, many dense terms)
+    are planned, not rejected (the GPU runs them in
+    test_gpu_parity.py::test_scheduling_variants_bitwise_equal)."""
     monkeypatch.setenv("PT_STAGES", str(stages))
     monkeypatch.setenv("PT_T_PIECES", "16")
     monkeypatch.setenv("PT_T_PIECES_CHAIN", "16")
     op = host_op(name)
     for kind, n_it in (("A", 0), ("M", 2), ("AM", 2)):
         st = op.plan_stats(kind, n_it) if n_it else op.plan_stats(kind)
-        assert 1 <= st["max_pieces"] <= 2 * stages
+        assert 1 <= st["max_pieces"] <= 48

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("case")
     ap.add_argument("kind", default="M", nargs="?")
     ap.add_argument("--n", type=int, default=40)
+    ap.add_argument("--dump", default=None, help="save the plan and the raw trace (npz)")
     args = ap.parse_args()
     meta, arr = load_case_arrays(ensure_case(args.case))
     op = DeviceOperator.from_arrays(meta, arr)
@@ -51,6 +52,9 @@ def main():
                                              rec.ctypes.data_as(C.POINTER(C.c_int64)), cap,
                                              C.byref(n)))
     r = rec[: n.value * TRW].reshape(n.value, TRW)
+    if args.dump:
+        chain = np.zeros(len(plan), dtype=np.int8)
+        np.savez_compressed(args.dump, plan=plan, trace=r)
     t0 = r[:, 6].min()
     us = lambda v: (v - t0) / 1e3  # noqa: E731
     grab, ready, done, cst, staged = us(r[:, 6]), us(r[:, 7]), us(r[:, 8]), us(r[:, 10]), us(r[:, 12])
