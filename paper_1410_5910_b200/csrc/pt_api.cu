@@ -60,10 +60,7 @@ struct DevProgram {
   DevItem* items = nullptr;
   int4* blob = nullptr;        // per-task metadata blobs (queue order)
   int64_t* blob_off = nullptr;  // task q: blob[blob_off[q] .. blob_off[q + 1])
-  int* qlist = nullptr;         // split queues (chain_ctas > 0): other tasks, then chain tasks
-  int qlen[2] = {0, 0};
   ~DevProgram() {
-    cudaFree(qlist);
     cudaFree(blob);
     cudaFree(blob_off);
     cudaFree(ents);
@@ -146,8 +143,6 @@ struct pt_handle {
   int n_stages = 4;        // operator ring stages
   int n_slots = EXEC_TSLOTS;  // task slots in use per CTA
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
-  int poll_stagger = 0;    // staggered polling of few counters (PT_POLL_STAGGER cycles; 0: off)
-  int chain_ctas = 0;      // CTAs reserved for the sweep-chain tasks (PT_CHAIN_CTAS; 0: one queue)
   std::unique_ptr<pt_gmres_ws> gws;
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
@@ -542,17 +537,6 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
   }
   for (int s : {SLOT_Y, SLOT_U1, SLOT_U2, SLOT_PRE, SLOT_T})
     if ((rc = ensure_slot(h, s, p->host.slot_elems[s]))) return rc;
-  if (h->chain_ctas > 0) {  // split queues: the sweep-chain tasks on their own CTAs
-    std::vector<int> other, chain;
-    for (size_t q = 0; q < p->host.tasks.size(); ++q)
-      (p->host.chain[q] ? chain : other).push_back((int)q);
-    if (!chain.empty() && !other.empty()) {
-      p->qlen[0] = (int)other.size();
-      p->qlen[1] = (int)chain.size();
-      other.insert(other.end(), chain.begin(), chain.end());
-      if ((rc = upload(&p->qlist, other))) return rc;
-    }
-  }
   // counters + queue head + exit ticket + chain queue head; zero between
   // launches (the executor's last CTA resets them)
   if (p->host.n_counters + 3 > h->ctr_cap) {
@@ -608,14 +592,9 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.n_stages = h->n_stages;
   a.n_slots = h->n_slots;
   a.poll_ns = h->poll_ns;
-  a.poll_stagger = h->poll_stagger;
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
   a.stop = stop;
-  a.qlist = p->qlist;
-  a.qlen0 = p->qlen[0];
-  a.qlen1 = p->qlen[1];
-  a.chain_ctas = h->chain_ctas;
   a.iter = im.iter;
   a.vbase = im.vbase;
   a.vstride = im.vstride;
@@ -866,7 +845,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
       EXEC_SRCS * (int64_t)sizeof(void*);
   h->slot_bytes = (h->slot_bytes + 127) / 128 * 128;
   // + the consumers' partials (the slot count is settled below)
-  size_t fixed = (size_t)EXEC_TSLOTS * h->slot_bytes + EXEC_CONSUMERS * sizeof(double2);
+  size_t fixed = (size_t)EXEC_TSLOTS * h->slot_bytes + EXEC_PART * sizeof(double2);
   // B200 figures for a host-only handle; the device's own otherwise
   int smem_sm = 233472, smem_blk = 232448, reserved = 1024, nsm = 148;
   cudaFuncAttributes fa{};
@@ -896,7 +875,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     min_slots = max_slots = std::max(1, std::min(EXEC_TSLOTS, std::atoi(e)));
   for (int ns = max_slots; ns >= min_slots; --ns) {
     h->n_slots = ns;
-    fixed = (size_t)ns * h->slot_bytes + EXEC_CONSUMERS * sizeof(double2);
+    fixed = (size_t)ns * h->slot_bytes + EXEC_PART * sizeof(double2);
     half = 0;
     for (int c = target; c >= 1 && half < need; --c) {
       ctas_sm = c;
@@ -950,9 +929,6 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_T_PIECES")) h->pp.t_pieces = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_ROW_CHUNK")) h->pp.row_chunk = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_POLL_NS")) h->poll_ns = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("PT_POLL_STAGGER")) h->poll_stagger = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("PT_CHAIN_CTAS"))
-    h->chain_ctas = std::min(std::max(0, std::atoi(e)), std::max(0, h->grid - 1));
   if (const char* e = std::getenv("PT_CHAIN_PIECE")) h->pp.chain_piece_elems = std::atoll(e);
   if (const char* e = std::getenv("PT_CHAIN_BOOST")) h->pp.chain_boost_us = std::atof(e);
   if (const char* e = std::getenv("PT_SIM_SLOTS")) h->pp.ctas = h->grid * std::max(1, std::atoi(e));

@@ -7,21 +7,19 @@
 
 namespace pt {
 
-// executor CTA (one per SM): 16 consumer warps + 2 producer warps (one per
+// executor CTA (one per SM): 16 consumer warps + 3 producer warps (one per
 // task slot)
 #ifndef PT_EXEC_CONSUMERS
 #define PT_EXEC_CONSUMERS 512
 #endif
 constexpr int EXEC_CONSUMERS = PT_EXEC_CONSUMERS;  // 512: one CTA per SM; 256: two
-#ifndef PT_EXEC_PRODUCERS
-#define PT_EXEC_PRODUCERS 3
-#endif
-constexpr int EXEC_PRODUCERS = PT_EXEC_PRODUCERS;  // = task slots
+constexpr int EXEC_PRODUCERS = 3;  // = task slots
 constexpr int EXEC_THREADS = EXEC_CONSUMERS + 32 * EXEC_PRODUCERS;
 constexpr int EXEC_WARPS = EXEC_CONSUMERS / 32;
 constexpr int EXEC_MAX_STAGES = 8;  // operator piece ring (TMA bulk copies); the
                                     // handle picks 2..8 stages from its smem budget
 constexpr int EXEC_TSLOTS = EXEC_PRODUCERS;  // task slots (metadata blob, staged vectors)
+constexpr int EXEC_PART = 256;      // consumer partial sums (complex), per CTA
 constexpr int EXEC_EPI = 16;        // epilogue rows per task slot (>= PLR_TILE, DENSE_RT_MAX)
 constexpr int EXEC_EPI_SRC = 6;     // epilogue source rows: init, eyes (<= 4), rhs
 constexpr int EXEC_TERMS = 16;      // term scales per task slot
@@ -116,7 +114,6 @@ struct ExecArgs {
   int32_t n_stages;          // ring stages (<= EXEC_MAX_STAGES)
   int32_t n_slots;           // task slots in use (2..EXEC_TSLOTS)
   int32_t poll_ns;           // back-off between dependency polls (0: spin)
-  int32_t poll_stagger;      // cycles between the staggered lanes' first polls (0: off)
   const int* stop;  // GMRES status stop flag: the whole launch is skipped once set
   // iteration-relative basis addressing (GMRES loop inside a graph):
   // if iter != nullptr, SLOT_IN = vbase + (*iter) * vstride, SLOT_OUT = SLOT_IN + vstride
@@ -126,12 +123,6 @@ struct ExecArgs {
   unsigned long long* trace;  // optional per-task timeline (debug/profiling)
   int n_tasks;
   int m;
-  // split queues (optional): CTAs [0, chain_ctas) take the sweep-chain tasks
-  // qlist[qlen0 ..), the others the remaining tasks qlist[0 .. qlen0), each
-  // list in queue order; head[0] / head[2] are their grab counters
-  const int* qlist;
-  int qlen0, qlen1;
-  int chain_ctas;
 };
 
 // TMA bulk prefetch of a contiguous range into L2 (no smem, no completion)

@@ -36,15 +36,6 @@ namespace pt {
 namespace {
 
 constexpr int CONSUMERS = EXEC_CONSUMERS;  // 512 threads, 16 warps
-#ifndef PT_YPLR_ILP
-#define PT_YPLR_ILP 1  // Y_PLR: two columns per iteration (c3 GMRES 19.45 -> 19.05 ms)
-#endif
-#ifndef PT_YPLR_UNROLL
-#define PT_YPLR_UNROLL 2
-#endif
-#ifndef PT_TPLR_ILP
-#define PT_TPLR_ILP 0
-#endif
 constexpr int CWARPS = CONSUMERS / 32;
 
 __shared__ double2* s_slot[N_SLOTS];
@@ -69,8 +60,6 @@ __shared__ volatile uint32_t s_next_pos; // first unreserved ring position
 // in_window.  Without the bound a producer several uses ahead (long tasks, or
 // more than two task slots) could read an older phase as complete.
 __shared__ volatile uint32_t s_consumed;
-__shared__ volatile unsigned s_seen[EXEC_TSLOTS];  // counters seen satisfied (staggered polling)
-constexpr int POLL_LANES = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -350,7 +339,39 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
   }
 }
 
-// Producer warp k: slot k, the CTA's slot uses i = k, k + 2, k + 4, ...
+// all 32 lanes: poll the task's dependency counters (in parallel) until every
+// producer group it reads has finished
+__device__ __forceinline__ void wait_deps(const ExecArgs& a, const DevTask& t, const Slot& sl, int lane) {
+  const DevWait* w = sl.waits();
+  const int nw = t.nwait;
+  bool ok = true;
+  for (int i = lane; i < nw; i += 32)
+    if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
+  ok = __all_sync(0xffffffffu, ok);
+  while (!ok) {
+    if (a.poll_ns > 0) __nanosleep(a.poll_ns);
+    ok = true;
+    for (int i = lane; i < nw; i += 32)
+      if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
+    ok = __all_sync(0xffffffffu, ok);
+  }
+}
+
+// lane 0: the task's metadata blob into slot k (one bulk copy); all lanes
+// wait for it (phase j of the slot's metadata barrier)
+__device__ __forceinline__ void fetch_blob(const ExecArgs& a, const Slot& sl, int k, int q, int j,
+                                           int lane) {
+  if (lane == 0) {
+    trace_mark(a, q, 0);
+    const int64_t o0 = __ldg(a.blob_off + q), o1 = __ldg(a.blob_off + q + 1);
+    const uint32_t bytes = (uint32_t)((o1 - o0) * 16);
+    bar_expect(&s_meta[k], bytes);
+    bulk_copy(sl.blob, a.blob + o0, bytes, &s_meta[k]);
+  }
+  bar_wait(&s_meta[k], j & 1);
+}
+
+// Producer warp k: slot k, the CTA's slot uses i = k, k + n_slots, ...
 __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
   const int lane = threadIdx.x & 31;
   const uint32_t ns = (uint32_t)L.n_stages;
@@ -358,7 +379,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
   int n_staged = 0;  // phases of this slot's staging barrier
   for (int j = 0;; ++j) {
     const int use = L.n_slots * j + k;
-    if (j > 0) {  // consumers done with use - 2: publish its outputs
+    if (j > 0) {  // consumers done with the previous use: publish its outputs
       bar_wait(&s_tempty[k], (j - 1) & 1);
       if (lane == 0) {  // release: the consumers' outputs before the count
         asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.ctr + sl.desc().signal)
@@ -370,13 +391,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     int q = 0;
     if (lane == 0) {
       while (s_grab_turn != use) __nanosleep(16);
-      if (a.qlist) {  // split queues: chain CTAs / the rest
-        const bool ch = (int)blockIdx.x < a.chain_ctas;
-        const int i = atomicAdd(a.head + (ch ? 2 : 0), 1);
-        q = i < (ch ? a.qlen1 : a.qlen0) ? a.qlist[(ch ? a.qlen0 : 0) + i] : a.n_tasks;
-      } else {
-        q = atomicAdd(a.head, 1);
-      }
+      q = atomicAdd(a.head, 1);
       s_grab_turn = use + 1;
     }
     q = __shfl_sync(0xffffffffu, q, 0);
@@ -389,15 +404,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
       }
       return;
     }
-    // the task's metadata blob: one bulk copy
-    if (lane == 0) {
-      trace_mark(a, q, 0);
-      const int64_t o0 = __ldg(a.blob_off + q), o1 = __ldg(a.blob_off + q + 1);
-      const uint32_t bytes = (uint32_t)((o1 - o0) * 16);
-      bar_expect(&s_meta[k], bytes);
-      bulk_copy(sl.blob, a.blob + o0, bytes, &s_meta[k]);
-    }
-    bar_wait(&s_meta[k], j & 1);
+    fetch_blob(a, sl, k, q, j, lane);
     const DevTask& t = sl.desc();
     parse_meta(t, sl, lane);
     int issued = 0;
@@ -414,44 +421,7 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
         ++issued;
       }
     }
-    {  // dependencies: the lanes poll the task's counters in parallel
-      const DevWait* w = sl.waits();
-      const int nw = t.nwait;
-      bool ok = true;
-      for (int i = lane; i < nw; i += 32)
-        if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
-      ok = __all_sync(0xffffffffu, ok);
-      if (!ok && a.poll_stagger > 0 && nw * POLL_LANES <= 32) {
-        // few counters: POLL_LANES lanes per counter, their polls staggered
-        // over one L2 round trip, so a counter is sampled every ~RTT/POLL_LANES
-        // instead of once per round trip; the first lane to see it satisfied
-        // (acquire) flags it for the others
-        if (lane == 0) s_seen[k] = 0u;
-        __syncwarp();
-        if (lane < nw * POLL_LANES) {
-          const int c = lane % nw, rank = lane / nw;
-          const long long t0 = clock64();
-          while (clock64() - t0 < (long long)rank * a.poll_stagger) {
-          }
-          for (;;) {
-            if ((s_seen[k] >> c) & 1u) break;
-            if (ld_acquire(a.ctr + w[c].ctr) >= w[c].val) {
-              atomicOr((unsigned*)&s_seen[k], 1u << c);
-              break;
-            }
-          }
-        }
-        __syncwarp();
-      } else {
-        while (!ok) {
-          if (a.poll_ns > 0) __nanosleep(a.poll_ns);
-          ok = true;
-          for (int i = lane; i < nw; i += 32)
-            if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
-          ok = __all_sync(0xffffffffu, ok);
-        }
-      }
-    }
+    wait_deps(a, t, sl, lane);
     if (lane == 0) trace_mark(a, q, 1);
     __syncwarp();
     stage_vectors(a, t, sl, k, n_staged, lane);
@@ -507,9 +477,13 @@ __device__ __forceinline__ void release_piece(const Layout& L, Ring& rg) {
   }
 }
 
-// T_PLR: t = scale * Vt (x_a [+ x_b]).  A group of L lanes (L = 8, 16 or 32
-// per piece, from the widest row) per Vt row: lane j sums columns j, j + L,
-// ... in order, then an xor tree over the group.
+// T_PLR: t = scale * Vt (x_a [+ x_b]).  Each Vt row is reduced by 32, 16 or
+// 8 lanes by its own length (t_lane_class); a piece's rows come in class
+// order, so they tile the consumer threads in aligned units of 8 lanes: a
+// 32-lane row is one warp, a 16-lane row half of one.  Lane j sums columns
+// j, j + 2L, ... and j + L, j + 3L, ... into two accumulators, added, then an
+// xor tree inside the row's lanes.  The summation order depends only on the
+// row's length, not on how rows were packed into pieces.
 __device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, const Slot& sl,
                                           const Layout& L, Ring& rg, int q) {
   double2* T = s_slot[SLOT_T];
@@ -517,36 +491,44 @@ __device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, c
   const DevItem* items = sl.items();
   for (int p = 0; p < t.npiece; ++p) {
     const DevPiece& pc = sl.pieces()[p];
-    const int lanes = pc.e0;
-    const int lsh = __ffs(lanes) - 1;  // lanes is 8, 16 or 32
-    const int sub = threadIdx.x & (lanes - 1);
+    const int n32 = pc.e0 & 1023, n16 = (pc.e0 >> 10) & 1023, n8 = (pc.e0 >> 20) & 1023;
+    const int u32 = 4 * n32, u16 = u32 + 2 * n16, units = u16 + n8;
     const double2* buf = wait_piece(a, L, rg, q, p);
-    for (int base = pc.f0; base < pc.f1; base += CONSUMERS >> lsh) {
-      const int r = base + (int)(threadIdx.x >> lsh);
-      double2 acc = make_double2(0.0, 0.0);
+    for (int u0 = 0; u0 < units; u0 += CONSUMERS / 8) {
+      const int u = u0 + (int)(threadIdx.x >> 3);
+      int row, lanes, lane;
+      if (u < u32) {
+        row = u >> 2, lanes = 32, lane = threadIdx.x & 31;
+      } else if (u < u16) {
+        row = n32 + ((u - u32) >> 1), lanes = 16, lane = threadIdx.x & 15;
+      } else {
+        row = n32 + n16 + (u - u16), lanes = 8, lane = threadIdx.x & 7;
+      }
+      double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
       DevItem it{};
-      if (r < pc.f1) {
-        it = items[r];
+      if (u < units) {
+        it = items[pc.f0 + row];
         const double2* V = buf + it.poff;
         const double2* x = sl.vec + it.lo;
-#if PT_TPLR_ILP
-        double2 acc2 = make_double2(0.0, 0.0);
-        int c = sub;
+        int c = lane;
         for (; c + lanes < it.n; c += 2 * lanes) {
-          acc = cfma(V[c], x[c], acc);
-          acc2 = cfma(V[c + lanes], x[c + lanes], acc2);
+          const double2 v0 = V[c], x0 = x[c], v1 = V[c + lanes], x1 = x[c + lanes];
+          acc = cfma(v0, x0, acc);
+          acc2 = cfma(v1, x1, acc2);
         }
         if (c < it.n) acc = cfma(V[c], x[c], acc);
         acc = cadd(acc, acc2);
-#else
-        for (int c = sub; c < it.n; c += lanes) acc = cfma(V[c], x[c], acc);
-#endif
       }
-      for (int o = lanes >> 1; o > 0; o >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double vx = __shfl_xor_sync(0xffffffffu, acc.x, o);
+        const double vy = __shfl_xor_sync(0xffffffffu, acc.y, o);
+        if (o < lanes) {
+          acc.x += vx;
+          acc.y += vy;
+        }
       }
-      if (r < pc.f1 && sub == 0) st_cg(T + t.tbase + r, cmul(sc, acc));
+      if (u < units && lane == 0) st_cg(T + t.tbase + it.hi, cmul(sc, acc));
     }
     release_piece(L, rg);
   }
@@ -567,7 +549,8 @@ __device__ __forceinline__ double2 epilogue_row(const DevTask& t, const Slot& sl
 }
 
 // Y_PLR: one PLR_TILE-row tile; thread = (row r, column group g); columns
-// f = g (mod 16) ascending; the 16 group sums per row added in group order.
+// f = g (mod 32) ascending, two per iteration into two accumulators; the
+// groups' sums per row are added in a fixed order.
 __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, const Slot& sl,
                                           const Layout& L, Ring& rg, int q) {
   constexpr int G = CONSUMERS / PLR_TILE;
@@ -578,56 +561,42 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
   for (int p = 0; p < t.npiece; ++p) {
     const DevPiece& pc = sl.pieces()[p];
     const double2* buf = wait_piece(a, L, rg, q, p);
-#if PT_YPLR_ILP
-    // PT_YPLR_UNROLL columns per iteration, alternately into two accumulators
-    // (independent loads and FMA chains), added at the end in a fixed order
     int f = pc.f0 + ((g - pc.f0) % G + G) % G;
-    for (; f + (PT_YPLR_UNROLL - 1) * G < pc.f1; f += PT_YPLR_UNROLL * G) {
-      DevItem it[PT_YPLR_UNROLL];
-      double2 tv[PT_YPLR_UNROLL], uv[PT_YPLR_UNROLL];
-#pragma unroll
-      for (int u = 0; u < PT_YPLR_UNROLL; ++u) {
-        it[u] = items[f + u * G];
-        tv[u] = sl.vec[f + u * G];
-      }
-#pragma unroll
-      for (int u = 0; u < PT_YPLR_UNROLL; ++u) {
-        const bool v = r >= it[u].lo && r < it[u].hi;
-        uv[u] = v ? buf[it[u].poff + (r - it[u].lo)] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < PT_YPLR_UNROLL; ++u) {
-        if (u & 1)
-          acc2 = cfma(uv[u], tv[u], acc2);
-        else
-          acc = cfma(uv[u], tv[u], acc);
-      }
+    for (; f + G < pc.f1; f += 2 * G) {
+      const DevItem i0 = items[f], i1 = items[f + G];
+      const double2 t0 = sl.vec[f], t1 = sl.vec[f + G];
+      const double2 u0 = r >= i0.lo && r < i0.hi ? buf[i0.poff + (r - i0.lo)] : make_double2(0.0, 0.0);
+      const double2 u1 = r >= i1.lo && r < i1.hi ? buf[i1.poff + (r - i1.lo)] : make_double2(0.0, 0.0);
+      acc = cfma(u0, t0, acc);
+      acc2 = cfma(u1, t1, acc2);
     }
-    for (; f < pc.f1; f += G) {
+    if (f < pc.f1) {
       const DevItem it = items[f];
       if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
     }
-#else
-    for (int f = pc.f0 + ((g - pc.f0) % G + G) % G; f < pc.f1; f += G) {
-      const DevItem it = items[f];
-      if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
-    }
-#endif
     release_piece(L, rg);
   }
+  // the two column groups of a warp (lanes r and r + 16) first, then the 16
+  // warp sums in four interleaved chains
+  double2 v = cadd(acc, acc2);
+  v.x += __shfl_xor_sync(0xffffffffu, v.x, 16);
+  v.y += __shfl_xor_sync(0xffffffffu, v.y, 16);
   double2* part = L.part();
-  part[g * PLR_TILE + r] = cadd(acc, acc2);
+  if ((threadIdx.x & 31) < PLR_TILE) part[(threadIdx.x >> 5) * PLR_TILE + r] = v;
   consumer_sync();
   if ((int)threadIdx.x < t.r1 - t.r0) {
-    double2 v = epilogue_row(t, sl, threadIdx.x);
+    double2 s4[4];
 #pragma unroll
-    for (int i = 0; i < G; ++i) v = cadd(v, part[i * PLR_TILE + threadIdx.x]);
-    st_cg(vptr_w(t.out) + t.r0 + threadIdx.x, v);
+    for (int i = 0; i < 4; ++i) s4[i] = part[i * PLR_TILE + threadIdx.x];
+#pragma unroll
+    for (int i = 4; i < CWARPS; ++i) s4[i & 3] = cadd(s4[i & 3], part[i * PLR_TILE + threadIdx.x]);
+    const double2 sum = cadd(cadd(s4[0], s4[1]), cadd(s4[2], s4[3]));
+    st_cg(vptr_w(t.out) + t.r0 + threadIdx.x, cadd(epilogue_row(t, sl, threadIdx.x), sum));
   }
 }
 
 // Y_DENSE: rows [r0, r1) (<= 4); piece p = rows of term p's kernel; columns
-// split over the 8 warps, per-warp scaled partials summed in warp order.
+// split over the warps, per-warp scaled partials summed in warp order.
 __device__ __forceinline__ void run_y_dense(const ExecArgs& a, const DevTask& t, const Slot& sl,
                                             const Layout& L, Ring& rg, int q) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

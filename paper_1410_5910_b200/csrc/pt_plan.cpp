@@ -135,11 +135,12 @@ class Builder {
             if (elems > pp_.half_elems) flag("a Vt row exceeds an operator stage");
             pc.elems = (int32_t)elems;
             pc.f1 = s1 - s0;
-            // lanes per Vt row in the consumers' dot products (8, 16 or 32)
-            int32_t widest = 0;
-            for (int32_t q = s0 + pc.f0; q < s1; ++q)
-              widest = std::max(widest, op_.slots[kp.slot0 + q].cols);
-            pc.e0 = widest <= 64 ? 8 : widest <= 128 ? 16 : 32;
+            // consumer lanes per Vt row: 32, 16 or 8 by the row's own length
+            // (~4-8 columns per lane); the piece's items are ordered by lane
+            // class below, counts packed in e0 (t_lane_classes)
+            int32_t ncls[3] = {0, 0, 0};
+            for (int32_t q = s0 + pc.f0; q < s1; ++q) ncls[t_lane_class(op_.slots[kp.slot0 + q].cols)]++;
+            pc.e0 = ncls[0] | (ncls[1] << 10) | (ncls[2] << 20);
             prog_.pieces.push_back(pc);
             total += elems;
           }
@@ -158,14 +159,17 @@ class Builder {
           tk.tbase = (int32_t)(dt.t_base + s0);
           for (int32_t p = 0; p < tk.npiece; ++p) {
             const DevPiece& pc = prog_.pieces[tk.piece0 + p];
-            for (int32_t q = pc.f0; q < pc.f1; ++q) {
-              const DevSlot& sl = op_.slots[kp.slot0 + s0 + q];
-              DevItem it{};
-              it.poff = (uint16_t)(sl.v_off - pc.src);
-              it.lo = (uint16_t)(sl.col_off - tk.c0);
-              it.hi = 0;
-              it.n = (uint16_t)sl.cols;
-              prog_.items.push_back(it);
+            for (int cls = 0; cls < 3; ++cls) {  // 32-lane rows, then 16, then 8
+              for (int32_t q = pc.f0; q < pc.f1; ++q) {
+                const DevSlot& sl = op_.slots[kp.slot0 + s0 + q];
+                if (t_lane_class(sl.cols) != cls) continue;
+                DevItem it{};
+                it.poff = (uint16_t)(sl.v_off - pc.src);
+                it.lo = (uint16_t)(sl.col_off - tk.c0);
+                it.hi = (uint16_t)q;  // the row's slot within the task
+                it.n = (uint16_t)sl.cols;
+                prog_.items.push_back(it);
+              }
             }
           }
           tk.nitem = (int32_t)prog_.items.size() - tk.item0;

@@ -60,7 +60,8 @@ struct DevWait {
 
 // One contiguous operator range a task stages into a ring stage with a TMA
 // bulk copy.  Y_PLR: whole rank columns [f0, f1) of the task's flat column
-// list.  T_PLR: slots [f0, f1) of the task, e0 = consumer lanes per Vt row.
+// list.  T_PLR: slots [f0, f1) of the task; e0 = its rows per consumer lane
+// class, n32 | n16 << 10 | n8 << 20 (the piece's items are in class order).
 // Y_DENSE: rows r0..r1 of term f0's kernel.
 struct DevPiece {
   int64_t src;     // element offset into the operator pool (dense or factors)
@@ -96,7 +97,7 @@ struct DevTask {
 // Per-task metadata item, 8 bytes, precomputed on the host.
 //  Y_PLR column: U data at its piece + poff, tile rows [lo, hi).
 //  T_PLR Vt row: data at its piece + poff, n columns, source at staged-slice
-//                offset lo; result to SLOT_T[tbase + row].
+//                offset lo; result to SLOT_T[tbase + hi].
 struct DevItem {
   uint16_t poff;
   uint16_t lo;
@@ -138,6 +139,13 @@ struct DevSlot {     // one Vt row, for the t-phase
   int64_t v_off;     // complex offset of this Vt row
   int32_t col_off, cols;
 };
+
+// T_PLR: a Vt row of n columns is reduced by 32, 16 or 8 consumer lanes
+// (class 0, 1, 2), about 4-8 columns per lane
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int t_lane_class(int n) { return n > 160 ? 0 : n > 64 ? 1 : 2; }
 
 constexpr int PLR_TILE = 16;           // rows of a Y_PLR task
 constexpr int ROW_CHUNK = 64;          // output rows published per producer group

@@ -318,8 +318,8 @@ VARIANTS = {
 @pytest.mark.parametrize("name", ["fx_plr", "fx_uneven", "fx_extrap_plr", "fx_extrap"])
 def test_scheduling_variants_bitwise_equal(cuda_ok, monkeypatch, name, variant):
     """Scheduling does not change results: with a different ring (two stages)
-    and tasks longer than the ring's parity window, the preconditioner apply
-    and the fused iteration are bitwise equal to the default executor's."""
+    or tasks longer than the ring's parity window, the applies and the fused
+    iteration are bitwise equal to the default executor's."""
     meta, arr, op = get(name)
     path = golden_path(name)
     for k, v in VARIANTS[variant].items():
