@@ -120,3 +120,45 @@ def test_warp_prefix_solve_agrees(cuda_ok, monkeypatch, case):
     warp.close()
     if not case.startswith("fx_"):
         loc.close()
+
+
+def volume_error(u, vol):
+    """Relative error of a volume field against the reference's record
+    (tools/make_volume_goldens.py): the full field, or for c3 every recorded
+    grid row, the norm and 16 seeded projections."""
+    if "ref_u" in vol:
+        return rel(u, np.asarray(vol["ref_u"]))
+    rows = np.asarray(vol["ref_u_row_index"])
+    ref_rows = np.asarray(vol["ref_u_rows"])
+    nrm = float(np.asarray(vol["ref_u_norm"])[0])
+    errs = [rel(u[rows], ref_rows), abs(np.linalg.norm(u) - nrm) / nrm]
+    from make_volume_goldens import projections  # tools/ (the generator's own vectors)
+    for p, ref in zip(projections(u.shape), np.asarray(vol["ref_u_proj"])):
+        errs.append(abs(np.vdot(p, u) - ref) / (np.linalg.norm(p) * nrm))
+    return max(errs)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_large_case_volume_matches_reference(cuda_ok, name):
+    """North-star bar at the BASELINE configurations: the volume field of the
+    whole device online stage (Newton traces, rhs, GMRES, reconstruction)
+    within 1e-8 of the reference's own solve_helmholtz (report.u,
+    local_solver.py:147-176), and the iteration count within +-1."""
+    import sys
+    from pathlib import Path
+    from paper_1410_5910_b200 import solver as S
+    from paper_1410_5910_b200.offline.build import ensure_case
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    vmeta, vol = load_case_arrays(golden_path(f"{name}_vol"))
+    path = ensure_case(name)
+    meta, _ = load_case_arrays(path)
+    state = S.OfflineState.from_case(path, local=True)
+    f = configs.config(name).sources[0][1]
+    rep = S.solve_helmholtz(None, None, None, f, state=state,
+                            precond=S.PreconditionerConfig(variant=meta.get("variant", "jump")),
+                            gmres=S.GmresConfig(rel_tol=meta["gmres_tol"]))
+    assert abs(rep.iterations - vmeta["iterations"]) <= 1
+    assert tuple(rep.u.shape) == tuple(vmeta["u_shape"])
+    assert volume_error(rep.u, vol) <= TRACE_TOL
+    state.local.close()
