@@ -166,6 +166,28 @@ def operator_checksums(meta, arrays):
     return out
 
 
+def compare_pinned_layers(meta, arrays, ref, rtol=1e-9):
+    """c4: the kernels of the layers the reference's own layer pipeline was run
+    on (tools/make_c4_ref.py) -- leaf structure identical, factor norms within
+    rtol.  Raises ValueError otherwise."""
+    lv = np.asarray(arrays["leaves"])
+    fac = np.asarray(arrays["factors"])
+    kern = np.asarray(ref["ck_pin_kernel"])
+    pin = np.asarray(ref["ck_pin_leaves"])
+    worst = 0.0
+    for k in np.unique(kern):
+        mine = lv[(lv[:, 0] == k) & (lv[:, 5] > 0)]
+        theirs = pin[kern == k]
+        if mine.shape[0] != theirs.shape[0] or not np.array_equal(mine[:, 1:6], theirs[:, :5].astype(np.int64)):
+            raise ValueError(f"kernel {k}: PLR leaf structure differs from the reference's")
+        for row, t in zip(mine, theirs):
+            nrm = np.linalg.norm(fac[row[6]:row[6] + row[3] * row[5]])
+            worst = max(worst, abs(nrm - t[5]) / max(t[5], 1e-300))
+    if worst > rtol:
+        raise ValueError(f"pinned kernels' factor norms differ from the reference's by {worst:.2e}")
+    return worst
+
+
 def compare_checksums(mine, ref, rtol=1e-9):
     """Raise ValueError if the operator differs from the reference's beyond rounding."""
     for k in ("entries", "perm"):
@@ -189,7 +211,8 @@ def compare_checksums(mine, ref, rtol=1e-9):
 
 
 REF_KEYS = ("ref_x", "ref_traces", "ref_hist", "probe_x", "probe_u", "probe_Ax", "probe_Mx",
-            "probe_M1x", "probe_sweep", "ref_index")
+            "probe_M1x", "probe_sweep", "ref_index", "probe_Ax_sub", "probe_Mx_sub",
+            "probe_Ax_norm", "probe_Mx_norm")
 
 
 def build_case(name, out_dir=None, workers=None, verify=True):
@@ -203,7 +226,10 @@ def build_case(name, out_dir=None, workers=None, verify=True):
     ref_path = GOLDEN / f"{name}_ref.ptc"
     if ref_path.exists():
         rmeta, rarr = read_case(ref_path, mmap=False)
-        if verify and name not in OPERATOR_OF:
+        if verify and name not in OPERATOR_OF and "ck_pin_kernel" in rarr:
+            meta["pinned_layers_rel_err"] = compare_pinned_layers(meta, arrays, rarr)
+            meta["verified_against_reference"] = "layers %s" % rmeta.get("pinned_layers")
+        elif verify and name not in OPERATOR_OF:
             compare_checksums(operator_checksums(meta, arrays), rarr)
             meta["verified_against_reference"] = True
         for k in REF_KEYS:
