@@ -16,8 +16,11 @@
  * reference raises RuntimeError, solver.py:255-258); pt_last_error()
  * returns the message of the last failure on the calling thread.
  *
- * Calls are stream-ordered on the given stream (NULL = legacy default);
- * a handle must not be used from two threads at once.
+ * Calls are stream-ordered on the given stream (NULL = legacy default).
+ * The programs of one handle share its dependency counters and scratch
+ * vectors, so a call on a different stream than the handle's previous call
+ * first waits for that call (an event); a handle must not be used from two
+ * threads at once.
  */
 #ifndef PT_B200_H
 #define PT_B200_H

@@ -143,6 +143,11 @@ struct pt_handle {
   int n_stages = 4;        // operator ring stages
   int n_slots = EXEC_TSLOTS;  // task slots in use per CTA
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
+  // Launch ordering across streams: every program launch shares the handle's
+  // counters, queue heads and scratch vectors, so a launch on another stream
+  // waits for the previous launch (its event) instead of racing it.
+  cudaEvent_t last_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
   std::unique_ptr<pt_gmres_ws> gws;
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
@@ -237,6 +242,7 @@ struct pt_handle {
       cudaEventDestroy(p.second);
     }
     for (auto e : ev_free) cudaEventDestroy(e);
+    if (last_ev) cudaEventDestroy(last_ev);
     drop_graphs();
     if (cap_stream) cudaStreamDestroy(cap_stream);
     cudaFree(gb);
@@ -559,6 +565,24 @@ struct IterMode {
   int64_t vstride = 0;
 };
 
+// before / after a launch of an executor program on stream s (see last_ev)
+int order_before(pt_handle* h, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return 0;  // graph nodes: ordered by the graph
+  if (h->last_ev && h->last_stream != s) CK(cudaStreamWaitEvent(s, h->last_ev, 0));
+  return 0;
+}
+int order_after(pt_handle* h, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return 0;
+  if (!h->last_ev) CK(cudaEventCreateWithFlags(&h->last_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(h->last_ev, s));
+  h->last_stream = s;
+  return 0;
+}
+
 int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, const double2* aux,
                 cudaStream_t s, const int* stop = nullptr, IterMode im = IterMode()) {
   if (p->host.tasks.empty()) return 0;
@@ -624,7 +648,10 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  int orc = order_before(h, s);
+  if (orc) return orc;
   CK(cudaLaunchKernelEx(&cfg, pt_exec_kernel, a));
+  if ((orc = order_after(h, s))) return orc;
   if (h->timing) {
     CK(cudaEventRecord(e1, s));
     h->ev_used.emplace_back(e0, e1);
@@ -1349,6 +1376,7 @@ int run_bprogram(pt_handle* h, DevProgram* p, const double2* in, double2* out, c
   a.iter = iter;
   a.vbase = vbase;
   a.vstride = vstride;
+  if (int orc = order_before(h, s)) return orc;
   CK(cudaMemsetAsync(B.ctr, 0, (p->host.n_counters + 1) * sizeof(int), s));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->timing) {
@@ -1363,6 +1391,7 @@ int run_bprogram(pt_handle* h, DevProgram* p, const double2* in, double2* out, c
     CK(cudaEventRecord(e0, s));
   }
   CK(bexec_launch(a, B.grid, B.rows, B.tcols, s));
+  if (int orc = order_after(h, s)) return orc;
   if (h->timing) {
     CK(cudaEventRecord(e1, s));
     h->ev_used.emplace_back(e0, e1);

@@ -333,3 +333,26 @@ def test_scheduling_variants_bitwise_equal(cuda_ok, monkeypatch, name, variant):
         assert np.array_equal(op.apply_AM(x, n_it=2), op2.apply_AM(x, n_it=2))
     finally:
         op2.close()
+
+
+@pytest.mark.parametrize("name", ["fx_plr", "fx_extrap"])
+def test_one_handle_on_two_streams(cuda_ok, name):
+    """Launches of one handle on different streams are ordered (they share the
+    handle's counters and scratch vectors): A on one stream and M, AM on
+    others, issued back to back, equal the applies run one by one."""
+    import torch
+    meta, arr, op = get(name)
+    x = torch.from_numpy(np.array(arr["probe_x"])).cuda()
+    ya_ref, zm_ref, zam_ref = op.apply_A(x), op.apply_M(x, n_it=2), op.apply_AM(x, n_it=2)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = [torch.empty_like(x) for _ in range(3)]
+    for _ in range(4):
+        with torch.cuda.stream(streams[0]):
+            op.apply_A(x, out=outs[0])
+        with torch.cuda.stream(streams[1]):
+            op.apply_M(x, n_it=2, out=outs[1])
+        with torch.cuda.stream(streams[2]):
+            op.apply_AM(x, n_it=2, out=outs[2])
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], ya_ref) and torch.equal(outs[1], zm_ref) and torch.equal(outs[2], zam_ref)
