@@ -296,6 +296,10 @@ int32_t pt_abi_version(void);
 /* number of kernels this library has launched since load (the nodes of
  * graph-resident solves are counted per execution) */
 int64_t pt_launch_count(void);
+/* 1 for the checked build (libpt_b200_check.so, -DPT_CHECK=1: the executor
+ * asserts its index/capacity invariants and bounds every spin loop, trapping
+ * with a record appended to pt_last_error()), 0 for the release build */
+int32_t pt_checked_build(void);
 /* algorithmic bytes of one A-apply / one n_it-sweep preconditioner apply
  * (distinct kernels read once) */
 int64_t pt_bytes_apply_A(const pt_handle *h);

@@ -14,6 +14,10 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("PT_B200_LIB", _HERE / "libpt_b200.so"))
+# PT_LIBRARY=check loads the checked build (libpt_b200_check.so: invariant
+# asserts and spin-loop watchdogs in the executor; csrc/Makefile `check`)
+if os.environ.get("PT_LIBRARY") == "check":
+    LIB_PATH = LIB_PATH.with_name("libpt_b200_check.so")
 
 PT_OK, PT_EINVAL, PT_ECUDA, PT_ENONFINITE = 0, -1, -2, -3
 PT_KERNEL_DENSE, PT_KERNEL_PLR = 0, 1
@@ -103,6 +107,7 @@ _SIGS = {
     "pt_last_error": (C.c_char_p, []),
     "pt_abi_version": (C.c_int32, []),
     "pt_launch_count": (C.c_int64, []),
+    "pt_checked_build": (C.c_int32, []),
     "pt_bytes_apply_A": (C.c_int64, [_VP]),
     "pt_bytes_apply_M": (C.c_int64, [_VP, C.c_int32]),
 }

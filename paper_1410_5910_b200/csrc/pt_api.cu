@@ -28,8 +28,16 @@ namespace {
 
 thread_local std::string g_err;
 
+// checked build: the executor's {code, task, value} record of the last
+// failed invariant (mapped host memory, readable after the launch traps)
+std::atomic<long long*> g_check_rec{nullptr};
+
 int fail(int code, const std::string& msg) {
   g_err = msg;
+  long long* r = g_check_rec.load();
+  if (r && r[0] != 0)
+    g_err += " [executor check " + std::to_string(r[0]) + " at task " + std::to_string(r[1]) +
+             ", value " + std::to_string(r[2]) + "]";
   return code;
 }
 
@@ -148,6 +156,9 @@ struct pt_handle {
   // waits for the previous launch (its event) instead of racing it.
   cudaEvent_t last_ev = nullptr;
   cudaStream_t last_stream = nullptr;
+  int64_t fac_elems = 0, dense_elems = 0;  // operator pool sizes (checked build)
+  long long* chk_host = nullptr;           // checked build: mapped {code, task, value}
+  long long* chk_dev = nullptr;
   std::unique_ptr<pt_gmres_ws> gws;
   double2* tmp = nullptr;
   double2* hb = nullptr;  // device staging for the *_host solve
@@ -243,6 +254,10 @@ struct pt_handle {
     }
     for (auto e : ev_free) cudaEventDestroy(e);
     if (last_ev) cudaEventDestroy(last_ev);
+    if (chk_host) {
+      if (g_check_rec.load() == chk_host) g_check_rec.store(nullptr);
+      cudaFreeHost(chk_host);
+    }
     drop_graphs();
     if (cap_stream) cudaStreamDestroy(cap_stream);
     cudaFree(gb);
@@ -422,6 +437,7 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
   if (h->host_only) return 0;
   int rc;
   if ((rc = upload(&h->fac, blob))) return rc;
+  h->fac_elems = (int64_t)blob.size();
   if ((rc = upload(&h->slots, op.slots))) return rc;
   if ((rc = upload(&h->kplr, op.kplr))) return rc;
   return 0;
@@ -618,6 +634,14 @@ int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, co
   a.poll_ns = h->poll_ns;
   a.n_tasks = (int)p->host.tasks.size();
   a.m = (int)h->op.m;
+  a.n_counters = p->host.n_counters;
+  a.fac_elems = h->fac_elems;
+  a.dense_elems = h->dense_elems;
+  a.t_elems = h->slot_cap[SLOT_T];
+  if (h->chk_host) {  // checked build (allocated at pt_create)
+    g_check_rec.store(h->chk_host);
+    a.err = h->chk_dev;
+  }
   a.stop = stop;
   a.iter = im.iter;
   a.vbase = im.vbase;
@@ -771,6 +795,7 @@ extern "C" {
 const char* pt_last_error(void) { return g_err.c_str(); }
 int32_t pt_abi_version(void) { return PT_ABI_VERSION; }
 int64_t pt_launch_count(void) { return pt::g_launches.load(); }
+int32_t pt_checked_build(void) { return PT_CHECK; }
 
 int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entries,
               const int64_t* perm, const double* dense, const pt_leaf* leaves, int64_t n_leaves,
@@ -813,6 +838,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
       if (!dense) return fail(PT_EINVAL, "dense kernel array missing");
       const size_t bytes = (size_t)op.nk * op.m * op.m * sizeof(double2);
       CK(cudaMalloc(&h->dense, bytes));
+      h->dense_elems = (int64_t)op.nk * op.m * op.m;
       CK(cudaMemcpy(h->dense, dense, bytes, cudaMemcpyHostToDevice));
     }
   } else {
@@ -964,6 +990,11 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
     h->pp.t_pieces_chain = std::max(1, std::atoi(e));
   if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
+  if (!host_only && pt_checked_build()) {  // the executor's failure record (mapped host memory)
+    CK(cudaHostAlloc(&h->chk_host, 4 * sizeof(long long), cudaHostAllocMapped));
+    std::memset(h->chk_host, 0, 4 * sizeof(long long));
+    CK(cudaHostGetDevicePointer(&h->chk_dev, h->chk_host, 0));
+  }
   *out = h.release();
   return 0;
 }

@@ -85,6 +85,26 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
   return v;
 }
 
+// Checked build (-DPT_CHECK=1, libpt_b200_check.so; PT_LIBRARY selects it):
+// the executor asserts its index and capacity invariants and bounds every
+// spin loop; a violation records (code, task, value) in ExecArgs::err and
+// traps, so the launch fails instead of corrupting memory or hanging.
+// compute-sanitizer is not available on the GPU pool; this is its stand-in.
+#ifndef PT_CHECK
+#define PT_CHECK 0
+#endif
+enum CheckCode : int {
+  CHK_PIECE_SIZE = 1,    // operator piece larger than a ring stage
+  CHK_PIECE_RANGE = 2,   // operator piece outside the operator pool
+  CHK_STAGE_VEC = 3,     // staged vectors beyond the slot's vector area
+  CHK_ITEM_RANGE = 4,    // an item addresses outside its ring stage
+  CHK_COUNTER = 5,       // counter index outside the program's counters
+  CHK_WINDOW = 6,        // ring parity window invariant broken
+  CHK_HANG = 7,          // a spin loop ran longer than the watchdog
+  CHK_EPI_ROWS = 8,      // more output rows than the epilogue staging holds
+  CHK_SLOT_T = 9,        // t-buffer index outside SLOT_T
+};
+
 struct ExecArgs {
   const DevTask* tasks;
   const DevTerm* terms;
@@ -123,6 +143,9 @@ struct ExecArgs {
   unsigned long long* trace;  // optional per-task timeline (debug/profiling)
   int n_tasks;
   int m;
+  int n_counters;
+  int64_t fac_elems, dense_elems, t_elems;  // pool and SLOT_T sizes (checked build)
+  long long* err;  // checked build: {code, task, value}
 };
 
 // TMA bulk prefetch of a contiguous range into L2 (no smem, no completion)

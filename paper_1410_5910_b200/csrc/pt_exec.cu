@@ -36,6 +36,36 @@ namespace pt {
 namespace {
 
 constexpr int CONSUMERS = EXEC_CONSUMERS;  // 512 threads, 16 warps
+
+// ---- checked build (PT_CHECK, see pt_device.cuh) --------------------------------
+#if PT_CHECK
+__shared__ long long* s_errp;
+__device__ __noinline__ void chk_fail(int code, long long q, long long val) {
+  if (s_errp && atomicCAS((unsigned long long*)s_errp, 0ull, (unsigned long long)code) == 0ull) {
+    s_errp[1] = q;
+    s_errp[2] = val;
+    __threadfence_system();
+  }
+  __trap();
+}
+#define CHK(cond, code, q, val)                      \
+  do {                                               \
+    if (!(cond)) chk_fail((code), (q), (long long)(val)); \
+  } while (0)
+// spin-loop watchdog: ~4e9 cycles (~2 s) in one wait is a hang
+#define SPIN_DECL const long long spin0_ = clock64()
+#define SPIN_CHECK(q) CHK(clock64() - spin0_ < 4000000000ll, CHK_HANG, (q), 0)
+#else
+#define CHK(cond, code, q, val) \
+  do {                          \
+  } while (0)
+#define SPIN_DECL \
+  do {            \
+  } while (0)
+#define SPIN_CHECK(q) \
+  do {                \
+  } while (0)
+#endif
 constexpr int CWARPS = CONSUMERS / 32;
 
 __shared__ double2* s_slot[N_SLOTS];
@@ -87,7 +117,9 @@ __device__ __forceinline__ bool bar_test(unsigned long long* b, uint32_t parity)
 }
 __device__ __forceinline__ void bar_wait(unsigned long long* b, uint32_t parity) {
   uint32_t done = 0;
+  SPIN_DECL;
   while (!done) {
+    SPIN_CHECK(-1);
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}"
@@ -208,6 +240,10 @@ __device__ __forceinline__ void issue_piece(const ExecArgs& a, const Layout& L, 
   const DevPiece& pc = sl.pieces()[p];
   const int s = pos % (uint32_t)L.n_stages;
   const uint32_t bytes = (uint32_t)pc.elems * (uint32_t)sizeof(double2);
+  CHK(pc.elems > 0 && pc.elems <= a.half_elems, CHK_PIECE_SIZE, q, pc.elems);
+  CHK(pc.src >= 0 && pc.src + pc.elems <=
+                         (sl.desc().type == TASK_Y_DENSE ? a.dense_elems : a.fac_elems),
+      CHK_PIECE_RANGE, q, pc.src);
   const double2* src = (sl.desc().type == TASK_Y_DENSE ? a.dense : a.fac) + pc.src;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   bar_expect(&s_full[s], bytes);
@@ -273,6 +309,8 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
   } else {
     for (int it = 0; it < t.nterm; ++it) bytes += (uint32_t)m * (sl.src[2 * it + 1] ? 2u : 1u);
   }
+  CHK(bytes <= (uint32_t)a.src_cap, CHK_STAGE_VEC, t.q, bytes);
+  CHK(nk == 0 || (nrows <= EXEC_EPI && nk <= EXEC_EPI_SRC), CHK_EPI_ROWS, t.q, nrows);
   bytes = (bytes + (uint32_t)(nk * nrows)) * (uint32_t)sizeof(double2);
   if (bytes == 0) return;
   const uint32_t phase = (uint32_t)(n_staged++ & 1);
@@ -293,6 +331,7 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
     const DevRun* runs = sl.runs();
     for (int i = lane; i < t.nrun; i += 32) {
       const DevRun r = runs[i];
+      CHK(r.f >= 0 && r.f + r.n <= t.nitem && r.t >= 0 && r.t + r.n <= a.t_elems, CHK_SLOT_T, t.q, r.t);
       bulk_copy(sl.vec + r.f, T + r.t, (uint32_t)r.n * (uint32_t)sizeof(double2), &s_stg[k]);
     }
     const DevSrcRun* sr = sl.sruns();  // dense leaves: source columns (both sources)
@@ -344,11 +383,14 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
 __device__ __forceinline__ void wait_deps(const ExecArgs& a, const DevTask& t, const Slot& sl, int lane) {
   const DevWait* w = sl.waits();
   const int nw = t.nwait;
+  for (int i = lane; i < nw; i += 32) CHK(w[i].ctr >= 0 && w[i].ctr < a.n_counters, CHK_COUNTER, t.q, w[i].ctr);
+  SPIN_DECL;
   bool ok = true;
   for (int i = lane; i < nw; i += 32)
     if (ld_acquire(a.ctr + w[i].ctr) < w[i].val) ok = false;
   ok = __all_sync(0xffffffffu, ok);
   while (!ok) {
+    SPIN_CHECK(t.q);
     if (a.poll_ns > 0) __nanosleep(a.poll_ns);
     ok = true;
     for (int i = lane; i < nw; i += 32)
@@ -382,6 +424,8 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     if (j > 0) {  // consumers done with the previous use: publish its outputs
       bar_wait(&s_tempty[k], (j - 1) & 1);
       if (lane == 0) {  // release: the consumers' outputs before the count
+        CHK(sl.desc().signal >= 0 && sl.desc().signal < a.n_counters, CHK_COUNTER, sl.desc().q,
+            sl.desc().signal);
         asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.ctr + sl.desc().signal)
                      : "memory");
       }
@@ -410,7 +454,13 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
     int issued = 0;
     uint32_t pos0 = 0;  // the use's first ring position
     if (lane == 0) {
-      while (s_resv_turn != use) __nanosleep(16);
+      {
+        SPIN_DECL;
+        while (s_resv_turn != use) {
+          SPIN_CHECK(q);
+          __nanosleep(16);
+        }
+      }
       pos0 = s_next_pos;
       s_next_pos = pos0 + (uint32_t)t.npiece;
       __threadfence_block();
@@ -433,7 +483,13 @@ __device__ void producer(const ExecArgs& a, const Layout& L, int k) {
       for (; issued < t.npiece; ++issued) {
         const uint32_t pos = pos0 + issued;
         if (pos >= ns) {
-          while (!in_window(pos, pos0, ns)) __nanosleep(32);
+          {
+            SPIN_DECL;
+            while (!in_window(pos, pos0, ns)) {
+              SPIN_CHECK(q);
+              __nanosleep(32);
+            }
+          }
           bar_wait(&s_empty[pos % ns], ((pos / ns) - 1) & 1);
         }
         issue_piece(a, L, sl, q, issued, pos);
@@ -508,6 +564,8 @@ __device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, c
       DevItem it{};
       if (u < units) {
         it = items[pc.f0 + row];
+        CHK(it.poff + it.n <= a.half_elems && it.lo + it.n <= a.src_cap &&
+                t.tbase + it.hi < a.t_elems, CHK_ITEM_RANGE, q, it.poff);
         const double2* V = buf + it.poff;
         const double2* x = sl.vec + it.lo;
         int c = lane;
@@ -564,6 +622,8 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
     int f = pc.f0 + ((g - pc.f0) % G + G) % G;
     for (; f + G < pc.f1; f += 2 * G) {
       const DevItem i0 = items[f], i1 = items[f + G];
+      CHK(i0.poff + (i0.hi - i0.lo) <= a.half_elems && i1.poff + (i1.hi - i1.lo) <= a.half_elems &&
+              i0.hi <= PLR_TILE && i1.hi <= PLR_TILE, CHK_ITEM_RANGE, q, f);
       const double2 t0 = sl.vec[f], t1 = sl.vec[f + G];
       const double2 u0 = r >= i0.lo && r < i0.hi ? buf[i0.poff + (r - i0.lo)] : make_double2(0.0, 0.0);
       const double2 u1 = r >= i1.lo && r < i1.hi ? buf[i1.poff + (r - i1.lo)] : make_double2(0.0, 0.0);
@@ -684,6 +744,9 @@ __global__ void __launch_bounds__(EXEC_THREADS, 512 / EXEC_CONSUMERS) pt_exec_ke
     s_slot[threadIdx.x] = p;
   }
   if (threadIdx.x == 0) {
+#if PT_CHECK
+    s_errp = a.err;
+#endif
     s_cyc_wait = s_cyc_sync = 0;
     s_resv_turn = 0;
     s_grab_turn = 0;

@@ -132,7 +132,7 @@ def volume_error(u, vol):
     ref_rows = np.asarray(vol["ref_u_rows"])
     nrm = float(np.asarray(vol["ref_u_norm"])[0])
     errs = [rel(u[rows], ref_rows), abs(np.linalg.norm(u) - nrm) / nrm]
-    from make_volume_goldens import projections  # tools/ (the generator's own vectors)
+    from volume_digest import projections  # the generator's own vectors
     for p, ref in zip(projections(u.shape), np.asarray(vol["ref_u_proj"])):
         errs.append(abs(np.vdot(p, u) - ref) / (np.linalg.norm(p) * nrm))
     return max(errs)
@@ -145,11 +145,8 @@ def test_large_case_volume_matches_reference(cuda_ok, name):
     whole device online stage (Newton traces, rhs, GMRES, reconstruction)
     within 1e-8 of the reference's own solve_helmholtz (report.u,
     local_solver.py:147-176), and the iteration count within +-1."""
-    import sys
-    from pathlib import Path
     from paper_1410_5910_b200 import solver as S
     from paper_1410_5910_b200.offline.build import ensure_case
-    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
     vmeta, vol = load_case_arrays(golden_path(f"{name}_vol"))
     path = ensure_case(name)
     meta, _ = load_case_arrays(path)

@@ -59,3 +59,18 @@ def test_struct_layouts_match_header():
     assert C.sizeof(nat.Leaf) == 64
     assert C.sizeof(nat.Layout) == 24
     assert C.sizeof(nat.GmresConfigC) == 16
+
+
+def test_checked_build_exports_the_same_boundary():
+    """libpt_b200_check.so (the executor with invariant asserts and spin-loop
+    watchdogs, the stand-in for compute-sanitizer on this pool) exports every
+    declared symbol and reports itself as checked; the release build does not."""
+    path = nat.LIB_PATH.with_name("libpt_b200_check.so")
+    if not path.exists():
+        pytest.skip("checked build not built (make -C paper_1410_5910_b200/csrc check)")
+    chk = C.CDLL(str(path))
+    missing = [n for n in declared() if not hasattr(chk, n)]
+    assert not missing, missing
+    chk.pt_checked_build.restype = C.c_int32
+    assert chk.pt_checked_build() == 1
+    assert nat.lib().pt_checked_build() == 0

@@ -8,16 +8,11 @@ reference's own offline_assemble + solve_helmholtz (solver.py:132-193,
 test_large_case_volume_matches_reference.
 """
 
-import sys
-from pathlib import Path
-
 import numpy as np
 import pytest
 
 from conftest import golden_path
 from paper_1410_5910_b200.operator import load_case_arrays
-
-sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
 
 
 @pytest.mark.parametrize("name,shape", [("c1", (200, 240)), ("c2", (400, 460)), ("c3", (800, 880))])
