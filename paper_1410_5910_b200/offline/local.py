@@ -78,31 +78,52 @@ def nd_order(nze, nxe, min_block=4, blocks=False):
     return p
 
 
-def factor_layer(op, nze, nxe, check=True):
+# SuperLU diagonal-pivot thresholds tried in order: 0 keeps the nested-dissection
+# order (every block a contiguous run, the device's block solve); the Helmholtz /
+# PML operators are indefinite, so a factorization whose residual check fails is
+# redone with threshold and then full partial pivoting (rows reordered: the
+# device falls back to its row-level solve).
+PIVOT_THRESHOLDS = (0.0, 0.1, 1.0)
+RESIDUAL_TOL = 1e-10
+
+
+def factor_layer(op, nze, nxe, check=True, thresholds=PIVOT_THRESHOLDS):
     """Factor one layer operator for the device: dict of CSR L, U and the
-    composed gathers q_in / q_out (see the module docstring)."""
+    composed gathers q_in / q_out (see the module docstring), plus the pivot
+    threshold that was used and the residual of a seeded solve."""
     op = sp.csc_matrix(op)
-    p, blocks = nd_order(nze, nxe, blocks=True)
+    p, blocks0 = nd_order(nze, nxe, blocks=True)
     a = sp.csc_matrix(op[p][:, p])
-    lu = spla.splu(a, permc_spec="NATURAL", diag_pivot_thresh=0.0)
     ident = np.arange(a.shape[0])
-    if not (np.array_equal(lu.perm_r, ident) and np.array_equal(lu.perm_c, ident)):
-        blocks = None  # SuperLU reordered: the blocks are no longer contiguous runs
-    L, U = lu.L.tocsr(), lu.U.tocsr()
-    L.sort_indices()
-    U.sort_indices()
-    inv_pr = np.argsort(lu.perm_r)
-    inv_p = np.argsort(p)
-    fac = {"L": L, "U": U, "q_in": p[inv_pr].astype(np.int64),
-           "q_out": np.asarray(lu.perm_c, dtype=np.int64)[inv_p], "block_ptr": blocks}
-    if check:
-        rng = np.random.default_rng(0)
-        b = rng.standard_normal(op.shape[0]) + 1j * rng.standard_normal(op.shape[0])
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(op.shape[0]) + 1j * rng.standard_normal(op.shape[0])
+    last = None
+    for thresh in thresholds:
+        try:
+            lu = spla.splu(a, permc_spec="NATURAL", diag_pivot_thresh=thresh)
+        except RuntimeError as exc:  # exactly singular pivot: pivot harder
+            last = f"threshold {thresh}: {exc}"
+            continue
+        blocks = blocks0
+        if not (np.array_equal(lu.perm_r, ident) and np.array_equal(lu.perm_c, ident)):
+            blocks = None  # SuperLU reordered: the blocks are no longer contiguous runs
+        L, U = lu.L.tocsr(), lu.U.tocsr()
+        L.sort_indices()
+        U.sort_indices()
+        inv_pr = np.argsort(lu.perm_r)
+        inv_p = np.argsort(p)
+        fac = {"L": L, "U": U, "q_in": p[inv_pr].astype(np.int64),
+               "q_out": np.asarray(lu.perm_c, dtype=np.int64)[inv_p], "block_ptr": blocks,
+               "pivot_thresh": thresh, "residual": None}
+        if not check:
+            return fac
         x = apply_factors(fac, b)
-        res = np.linalg.norm(op @ x - b) / np.linalg.norm(b)
-        if not res < 1e-10:
-            raise RuntimeError(f"nested-dissection factorization inaccurate (residual {res:.2e})")
-    return fac
+        res = float(np.linalg.norm(op @ x - b) / np.linalg.norm(b))
+        fac["residual"] = res
+        if res < RESIDUAL_TOL:
+            return fac
+        last = f"threshold {thresh}: residual {res:.2e}"
+    raise RuntimeError(f"layer factorization inaccurate at every pivot threshold ({last})")
 
 
 def apply_factors(fac, b):

@@ -229,7 +229,9 @@ class DeviceOperator:
         return self._ret(z, host)
 
     def gmres(self, b, rel_tol=1e-7, max_iter=100, n_it=2, out=None):
-        """Device GMRES; returns (x, report dict).  One host sync per iteration."""
+        """Device GMRES; returns (x, report dict).  The whole solve is one CUDA
+        graph (conditional WHILE node): the host synchronises once per solve
+        (PT_GRAPH=0: host-driven, one sync per batch of iterations)."""
         bd, host = self._dev_vec(b, "b")
         x = self._out(out, host)
         cfg = nat.GmresConfigC(float(rel_tol), int(max_iter), int(n_it))

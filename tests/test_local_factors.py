@@ -81,3 +81,30 @@ def test_nd_blocks_are_contiguous_runs_of_the_factor():
         L = fac["L"].tocoo()
         blk = np.searchsorted(bp, np.arange(L.shape[0]), side="right") - 1
         assert np.all(blk[L.col] <= blk[L.row])
+
+
+def test_pivoting_fallback_on_an_unstable_diagonal():
+    """Helmholtz/PML layer operators are indefinite: when the diagonal-pivot
+    (nested-dissection preserving) factorization fails its residual check,
+    factor_layer redoes it with threshold / partial pivoting and reports the
+    threshold and residual; the device then uses the row-level solve
+    (block_ptr None when rows were reordered)."""
+    import scipy.sparse as sp
+    n = 4 * 5
+    rng = np.random.default_rng(11)
+    # tiny diagonal, O(1) couplings: the unpivoted elimination blows up
+    a = sp.random(n, n, density=0.3, random_state=3, format="csc") * 1.0
+    a = a + sp.diags(np.full(n, 1e-13)) + sp.diags(np.ones(n - 1), 1) + sp.diags(np.ones(n - 1), -1)
+    a = sp.csc_matrix(a.astype(np.complex128))
+    fac = factor_layer(a, 4, 5)
+    assert fac["residual"] < 1e-10
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert np.linalg.norm(a @ apply_factors(fac, b) - b) <= 1e-10 * np.linalg.norm(b)
+    # the nested-dissection-preserving pass alone is rejected loudly
+    with pytest.raises(RuntimeError):
+        factor_layer(a, 4, 5, thresholds=(0.0,))
+
+
+def test_regular_layers_keep_the_dissection_order():
+    facs, geo = build_local("fx_plr", workers=1)
+    assert all(f["pivot_thresh"] == 0.0 and f["residual"] < 1e-10 for f in facs)
