@@ -230,8 +230,9 @@ int pt_exec_info(const pt_handle *h, int32_t *grid, int64_t *smem_bytes,
 int pt_plan_stats(pt_handle *h, int32_t kind, int32_t n_it, int64_t *stats);
 
 /* Host-side task list of one program (profiling aid): rec[PT_TASK_WORDS*q
- * ...] = {type, signal counter, nwait, pieces, r0, r1, out slot, out offset,
- * (counter, target) of the first 8 waits (-1: none)} in queue order. */
+ * ...] = {type, signal counter, nwait | on-sweep-chain << 16, pieces, r0, r1,
+ * out slot | items << 8, staged operator elements, (counter, target) of the
+ * first 8 waits (-1: none)} in queue order. */
 #define PT_TASK_WORDS 24
 int pt_plan_tasks(pt_handle *h, int32_t kind, int32_t n_it, int32_t *rec,
                   int64_t cap, int64_t *n_out);

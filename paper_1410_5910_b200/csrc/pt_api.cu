@@ -1980,12 +1980,14 @@ int pt_plan_tasks(pt_handle* h, int32_t kind, int32_t n_it, int32_t* rec, int64_
     int32_t* r = rec + PT_TASK_WORDS * q;
     r[0] = t.type;
     r[1] = t.signal;
-    r[2] = t.nwait;
+    r[2] = t.nwait | ((q < (int64_t)pg.chain.size() && pg.chain[q]) ? 1 << 16 : 0);
     r[3] = t.npiece;
     r[4] = t.r0;
     r[5] = t.r1;
-    r[6] = t.out.slot;
-    r[7] = (int32_t)t.out.off;
+    int64_t elems = 0;  // operator elements the task stages
+    for (int32_t i = 0; i < t.npiece; ++i) elems += pg.pieces[t.piece0 + i].elems;
+    r[6] = t.out.slot | (t.nitem << 8);
+    r[7] = (int32_t)elems;
     for (int i = 0; i < 8; ++i) {
       const bool has = i < t.nwait;
       r[8 + 2 * i] = has ? pg.waits[t.wait0 + i].ctr : -1;
