@@ -150,6 +150,7 @@ struct pt_handle {
   int64_t slot_bytes = 0;  // bytes of one task slot
   int n_stages = 4;        // operator ring stages
   int n_slots = EXEC_TSLOTS;  // task slots in use per CTA
+  int api_fmt = 0;         // the kernel format pt_create was given (op.fmt is the executor's storage)
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
   // Launch ordering across streams: every program launch shares the handle's
   // counters, queue heads and scratch vectors, so a launch on another stream
@@ -439,6 +440,68 @@ int build_plr_tables(pt_handle* h, const pt_leaf* leaves, int64_t n_leaves, cons
   if ((rc = upload(&h->fac, blob))) return rc;
   h->fac_elems = (int64_t)blob.size();
   if ((rc = upload(&h->slots, op.slots))) return rc;
+  if ((rc = upload(&h->kplr, op.kplr))) return rc;
+  return 0;
+}
+
+// Dense kernels for the single-source executor: the same tile-major storage
+// as a PLR kernel's dense leaves (one full leaf per kernel: for each 16-row
+// tile, column by column, the tile's rows), so dense operators run the
+// 16-row Y_PLR tasks -- a task stages its source vectors once per 16 output
+// rows, and the consumers read conflict-free 16-row columns.  The row-major
+// pool stays for the batched executor.  Same bytes as the m x m kernels.
+int build_dense_tiles(pt_handle* h, const double* dense) {
+  Operator& op = h->op;
+  const int64_t m = op.m;
+  const int64_t ntiles = (m + PLR_TILE - 1) / PLR_TILE;
+  std::vector<double2> blob;
+  blob.reserve((size_t)op.nk * m * m + 8 * (size_t)op.nk * ntiles);
+  op.kplr.assign(op.nk, DevKernelPLR{});
+  op.nslot.assign(op.nk, 0);
+  for (int k = 0; k < op.nk; ++k) {
+    const double* K = h->host_only ? nullptr : dense + 2 * (size_t)k * m * m;
+    DevKernelPLR& kp = op.kplr[k];
+    kp.leaf0 = (int32_t)op.leaves.size();
+    kp.slot0 = (int32_t)op.slots.size();
+    kp.nleaf = 1;
+    kp.nslot = 0;
+    DevLeaf dl{};
+    dl.rows = dl.cols = dl.rank = (int32_t)m;
+    dl.slot0 = -1;
+    dl.v_off = (int64_t)blob.size();
+    op.leaves.push_back(dl);
+    kp.tile0 = (int32_t)op.tile_ptr.size();
+    for (int64_t t = 0; t < ntiles; ++t) {
+      while (blob.size() % 8) blob.push_back(make_double2(0.0, 0.0));
+      op.tile_ptr.push_back((int32_t)op.tile_ent.size());
+      op.tile_chunk.push_back((int64_t)blob.size());
+      const int64_t lo = t * PLR_TILE, hi = std::min<int64_t>(m, lo + PLR_TILE);
+      DevTileEntry te{};
+      te.u0 = (int64_t)blob.size();
+      te.t0 = -1;
+      te.stride = (int32_t)(hi - lo);
+      te.rank = (int32_t)m;
+      te.pre = 0;
+      te.lo = 0;
+      te.hi = (int16_t)(hi - lo);
+      if (K) {
+        for (int64_t c = 0; c < m; ++c)
+          for (int64_t r = lo; r < hi; ++r)
+            blob.push_back(make_double2(K[2 * (r * m + c)], K[2 * (r * m + c) + 1]));
+      } else {
+        blob.resize(blob.size() + (size_t)((hi - lo) * m));
+      }
+      op.tile_ent.push_back(te);
+    }
+    op.tile_ptr.push_back((int32_t)op.tile_ent.size());
+    op.tile_chunk.push_back((int64_t)blob.size());
+  }
+  if (op.tile_ent.empty()) op.tile_ent.push_back(DevTileEntry{});
+  if (blob.empty()) blob.push_back(make_double2(0.0, 0.0));
+  h->fac_elems = (int64_t)blob.size();
+  if (h->host_only) return 0;
+  int rc;
+  if ((rc = upload(&h->fac, blob))) return rc;
   if ((rc = upload(&h->kplr, op.kplr))) return rc;
   return 0;
 }
@@ -832,6 +895,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (!validate_operator(op, err)) return fail(PT_EINVAL, err);
   h->sweep_err = sweep_diagonal_error(op);
   int rc;
+  h->api_fmt = op.fmt;
   if (op.fmt == PT_KERNEL_DENSE) {
     op.kernel_bytes.assign(op.nk, 16 * op.m * op.m);
     if (op.nk > 0 && !host_only) {
@@ -841,10 +905,19 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
       h->dense_elems = (int64_t)op.nk * op.m * op.m;
       CK(cudaMemcpy(h->dense, dense, bytes, cudaMemcpyHostToDevice));
     }
+    // the single-source executor streams dense kernels tile-major, as the
+    // dense leaves of a PLR kernel (PT_DENSE_TILES=0: row-major Y_DENSE tasks)
+    bool tiles = true;
+    if (const char* e = std::getenv("PT_DENSE_TILES")) tiles = std::atoi(e) != 0;
+    if (tiles) {
+      if ((rc = build_dense_tiles(h.get(), dense))) return rc;
+      op.fmt = PT_KERNEL_PLR;
+    }
   } else {
     if (n_leaves > 0 && (!leaves || !factors)) return fail(PT_EINVAL, "PLR tables missing");
     if ((rc = build_plr_tables(h.get(), leaves, n_leaves, factors, n_factor_complex))) return rc;
   }
+  if (const char* e = std::getenv("PT_BLOCK_TERMS")) h->pp.max_block_terms = std::max(0, std::atoi(e));
   // Shared memory per CTA: [EXEC_STAGES operator ring stages][EXEC_TSLOTS task
   // slots: descriptor, items, staged vectors, epilogue rows, term scales]
   // [consumer partials].  The stages take what is left after the fixed part
@@ -860,6 +933,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     // item per Vt row (<= MAX_T_SLOTS) and a source slice (<= tcols_cap)
     PlanParams probe;
     probe.half_elems = (int64_t)1 << 30;
+    probe.max_block_terms = h->pp.max_block_terms;
     int64_t ycols = 0, yvec = 0;
     for (const Program& pg : {build_apply_A(op, probe), build_apply_M(op, 2, probe),
                               build_gs_sweep(op, probe)})
@@ -1298,6 +1372,8 @@ int batch_init(pt_handle* h) {
   B.grid = bexec_grid(h->device, B.rows, B.tcols);
   if (B.grid <= 0) return fail(PT_ECUDA, "batched executor does not fit on an SM");
   B.pp = h->pp;
+  B.pp.force_dense = true;  // Y_DENSE tasks over the row-major dense pool
+  B.pp.max_block_terms = 0;
   B.pp.ctas = B.grid;
   B.pp.dense_rows_per_task = B.rows;
   B.pp.row_chunk = B.rows;  // every task its own producer group: finest dependencies
@@ -1734,7 +1810,7 @@ int pt_gmres_batch(pt_handle* h, const double* b, double* x, int32_t nrhs,
   if (rc) return rc;
   if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
   const int64_t N = h->N();
-  if (h->op.fmt == PT_KERNEL_DENSE && nrhs > 1 && !std::getenv("PT_BATCH_SEQ")) {
+  if (h->api_fmt == PT_KERNEL_DENSE && nrhs > 1 && !std::getenv("PT_BATCH_SEQ")) {
     DeviceGuard guard(h->device);
     return gmres_batched(h, (const double2*)b, (double2*)x, nrhs, false, cfg, reports,
                          (cudaStream_t)stream);
@@ -1754,7 +1830,7 @@ int pt_gmres_batch_host(pt_handle* h, const double* b_host, double* x_host, int3
   if (rc) return rc;
   if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
   const int64_t N = h->N();
-  if (h->op.fmt == PT_KERNEL_DENSE && nrhs > 1 && !std::getenv("PT_BATCH_SEQ")) {
+  if (h->api_fmt == PT_KERNEL_DENSE && nrhs > 1 && !std::getenv("PT_BATCH_SEQ")) {
     DeviceGuard guard(h->device);
     return gmres_batched(h, (const double2*)b_host, (double2*)x_host, nrhs, true, cfg, reports,
                          (cudaStream_t)stream);
@@ -1770,7 +1846,7 @@ int pt_gmres_batch_host(pt_handle* h, const double* b_host, double* x_host, int3
 int pt_apply_A_batch(pt_handle* h, const double* x, double* y, int32_t nrhs, pt_stream stream) {
   if (h && h->host_only) return fail(PT_EINVAL, "plan-only handle (PT_DEVICE_HOST)");
   if (!h || !x || !y || nrhs < 0) return fail(PT_EINVAL, "bad argument");
-  if (h->op.fmt != PT_KERNEL_DENSE) return fail(PT_EINVAL, "batched applies need a dense operator");
+  if (h->api_fmt != PT_KERNEL_DENSE) return fail(PT_EINVAL, "batched applies need a dense operator");
   DeviceGuard guard(h->device);
   return apply_batched(h, "A", 0, (const double2*)x, (double2*)y, nrhs, (cudaStream_t)stream);
 }
@@ -1781,7 +1857,7 @@ int pt_apply_M_batch(pt_handle* h, const double* r, double* z, int32_t nrhs, int
   if (!h || !r || !z || nrhs < 0) return fail(PT_EINVAL, "bad argument");
   if (n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
   if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
-  if (h->op.fmt != PT_KERNEL_DENSE) return fail(PT_EINVAL, "batched applies need a dense operator");
+  if (h->api_fmt != PT_KERNEL_DENSE) return fail(PT_EINVAL, "batched applies need a dense operator");
   DeviceGuard guard(h->device);
   return apply_batched(h, "M", n_it, (const double2*)r, (double2*)z, nrhs, (cudaStream_t)stream);
 }

@@ -74,8 +74,15 @@ class Builder {
     // waits every output task of the block has (t-vectors, dense sources);
     // the row-local inputs (eyes, init, rhs) are added per task
     std::vector<int> waits;
+    // producers of init as they are now: a block that accumulates in place
+    // (init == out) replaces them below
+    std::vector<RowGroup> init_prod;
+    if (has_init) {
+      auto it = producer_.find(std::make_pair(init.slot, init.off));
+      if (it != producer_.end()) init_prod = it->second;
+    }
     const int32_t term0 = (int32_t)prog_.terms.size();
-    const bool plr = op_.fmt == 1 && !terms.empty();
+    const bool plr = op_.fmt == 1 && !pp_.force_dense && !terms.empty();
     double ybytes = 0.0;
     for (const TermSpec& t : terms) {
       DevTerm dt{};
@@ -302,7 +309,10 @@ class Builder {
       for (int g2 : dense_waits)
         if (std::find(tw.begin(), tw.end(), g2) == tw.end()) tw.push_back(g2);
       for (const EyeSpec& e : eyes) add_wait_rows(tw, e.src, tk.r0, tk.r1);
-      if (has_init) add_wait_rows(tw, init, tk.r0, tk.r1);
+      if (has_init)
+        for (const RowGroup& rg : init_prod)
+          if (rg.lo < tk.r1 && tk.r0 < rg.hi && std::find(tw.begin(), tw.end(), rg.g) == tw.end())
+            tw.push_back(rg.g);
       if (has_rhs) add_wait_rows(tw, rhs, tk.r0, tk.r1);
       push_task(tk, tw, g, ybytes * double(tk.r1 - tk.r0) / double(m));
     }
@@ -512,7 +522,26 @@ void emit_A(Builder& b, const Operator& op, int32_t in_slot, int32_t out_slot) {
       }
       if (e.e_re != 0.0 || e.e_im != 0.0) eyes.push_back(EyeSpec{e.e_re, e.e_im, src});
     }
-    b.emit_block(ref(out_slot, i * m), terms, eyes, false, VecRef{}, false, VecRef{}, 0.0);
+    const int cap = b.params().max_block_terms;
+    if (op.fmt == 1 && !b.params().force_dense && cap > 0 && (int)terms.size() > cap) {
+      // partial sums of at most `cap` terms, accumulated in place; heavy and
+      // light kernels paired so the partial tasks stage about the same
+      std::sort(terms.begin(), terms.end(), [&](const TermSpec& x, const TermSpec& y) {
+        return op.kernel_bytes[x.kernel] > op.kernel_bytes[y.kernel];
+      });
+      const int nparts = ((int)terms.size() + cap - 1) / cap;
+      std::vector<std::vector<TermSpec>> parts(nparts);
+      for (size_t t = 0; t < terms.size(); ++t) {
+        const size_t round = t / nparts, pos = t % nparts;
+        parts[round % 2 == 0 ? pos : nparts - 1 - pos].push_back(terms[t]);
+      }
+      const VecRef out = ref(out_slot, i * m);
+      for (int p = 0; p < nparts; ++p)
+        b.emit_block(out, parts[p], p == nparts - 1 ? eyes : std::vector<EyeSpec>(), p > 0, out, false,
+                     VecRef{}, 0.0);
+    } else {
+      b.emit_block(ref(out_slot, i * m), terms, eyes, false, VecRef{}, false, VecRef{}, 0.0);
+    }
   }
   b.end_stage();
 }

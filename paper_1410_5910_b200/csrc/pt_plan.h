@@ -75,6 +75,10 @@ struct PlanParams {
   double chain_boost_us = 0.0;   // queue priority bonus of sweep-chain tasks
   int64_t chain_piece_elems = 0; // T_PLR piece cap on the sweep chain (0: a stage)
   int64_t item_cap = 1 << 20;    // metadata items a task slot holds
+  int max_block_terms = 0;       // A-apply: kernel terms per output task (0: all; else a block row is
+                                 // emitted as partial sums of at most this many terms: smaller task slots)
+  bool force_dense = false;      // plan row-major dense tasks (Y_DENSE) whatever the operator's storage
+                                 // (the batched executor streams the row-major dense pool)
   int64_t tcols_cap = MAX_TCOLS; // source columns a T_PLR task stages
 };
 

@@ -39,7 +39,8 @@ def test_every_program_plans(name):
         assert st["t_plr"] + st["y_plr"] + st["y_dense"] == st["tasks"]
         assert st["counters"] >= 1
         if op.kernel_format == "dense":
-            assert st["t_plr"] == st["y_plr"] == st["items"] == 0
+            # dense kernels run as tile-major dense leaves: 16-row Y tasks, no Vt work
+            assert st["t_plr"] == 0
         else:
             assert st["t_plr"] > 0 and st["y_plr"] > 0
 
