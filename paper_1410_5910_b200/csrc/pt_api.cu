@@ -1056,11 +1056,6 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_T_PIECES")) h->pp.t_pieces = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_ROW_CHUNK")) h->pp.row_chunk = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PT_POLL_NS")) h->poll_ns = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("PT_CHAIN_PIECE")) h->pp.chain_piece_elems = std::atoll(e);
-  if (const char* e = std::getenv("PT_CHAIN_BOOST")) h->pp.chain_boost_us = std::atof(e);
-  if (const char* e = std::getenv("PT_SIM_SLOTS")) h->pp.ctas = h->grid * std::max(1, std::atoi(e));
-  if (const char* e = std::getenv("PT_TASK_US")) h->pp.task_us = std::atof(e);
-  if (const char* e = std::getenv("PT_CTA_GBS")) h->pp.cta_gbs = std::atof(e);
   if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
     h->pp.t_pieces_chain = std::max(1, std::atoi(e));
   if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
@@ -1382,8 +1377,6 @@ int batch_init(pt_handle* h) {
   // FP64-bound rate of one CTA (BW/2 flop per kernel byte)
   B.pp.task_us = 1.0;
   B.pp.cta_gbs = 2.5;
-  if (const char* e = std::getenv("PT_BATCH_CTA_GBS")) B.pp.cta_gbs = std::atof(e);
-  if (const char* e = std::getenv("PT_BATCH_BOOST")) B.pp.chain_boost_us = std::atof(e);
   const size_t bytes = (size_t)h->N() * BW * sizeof(double2);
   CK(cudaMalloc(&B.b, bytes));
   CK(cudaMalloc(&B.x, bytes));

@@ -608,20 +608,11 @@ cudaError_t gm_arnoldi_step(const GmresDev& g, double rel_tol, int max_iter,
   cfg.blockDim = dim3(ARN_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (g.l2_window > 0) {
-    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[1].val.accessPolicyWindow.base_ptr = g.V;
-    attr[1].val.accessPolicyWindow.num_bytes = g.l2_window;
-    attr[1].val.accessPolicyWindow.hitRatio = g.l2_hit;
-    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.numAttrs = 2;
-  }
   return cudaLaunchKernelEx(&cfg, k_arnoldi, g, rel_tol, max_iter, cond);
 }
 
@@ -630,31 +621,6 @@ cudaError_t gm_arnoldi_setup(GmresDev& g, int device) {
   cudaError_t e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return e;
   g.arn_blocks = nsm < ARN_MAX_BLOCKS ? nsm : ARN_MAX_BLOCKS;
-  g.l2_window = 0;
-  g.l2_hit = 0.f;
-  {  // basis kept in L2 across iterations (PT_ARN_L2=1; off by default: at c3
-     // the staging phase gains ~0.7 us but the executor loses more, solve
-     // 18.32 -> 18.39 ms)
-    const char* env = std::getenv("PT_ARN_L2");
-    int persist = 0, window = 0;
-    if (env && env[0] == '1' &&
-        cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess &&
-        cudaDeviceGetAttribute(&window, cudaDevAttrMaxAccessPolicyWindowSize, device) == cudaSuccess &&
-        persist > 0 && window > 0) {
-      const size_t vbytes = (size_t)(g.max_iter + 1) * (size_t)g.n * sizeof(double2);
-      const size_t win = std::min(vbytes, (size_t)window);
-      size_t cur = 0;
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-      const size_t want = std::min(win, (size_t)persist);
-      if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-      if (cur > 0) {
-        g.l2_window = win;
-        g.l2_hit = (float)std::min(1.0, (double)cur / (double)win);
-      }
-    }
-    cudaGetLastError();
-  }
   const int64_t chunk = (g.n + g.arn_blocks - 1) / g.arn_blocks;
   int maxdyn = 0;
   e = cudaDeviceGetAttribute(&maxdyn, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);

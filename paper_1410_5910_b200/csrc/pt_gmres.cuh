@@ -53,11 +53,6 @@ struct GmresDev {
   DevStatus* st;
   int* ticket;        // last-block tickets of the fused reductions (3)
   int* nonfinite;
-  // L2 persistence of the basis for the Arnoldi step (host side; 0: off):
-  // V is re-read every iteration while the operator stream in between
-  // would evict it
-  size_t l2_window;
-  float l2_hit;
 };
 
 // launch helpers (pt_gmres.cu); all stream-ordered and graph-capturable.

@@ -61,12 +61,8 @@ class Builder {
   // the blocks emitted next are on a sweep's dependency chain (queue priority)
   bool chain_now = false;
   const PlanParams& params() const { return pp_; }
-  // operator elements per T_PLR piece for the blocks emitted next (smaller
-  // on the sweep chain: a chain task's compute is on the critical path)
-  int64_t t_piece_cap() const {
-    return chain_now && pp_.chain_piece_elems > 0 ? std::min(pp_.half_elems, pp_.chain_piece_elems)
-                                                  : pp_.half_elems;
-  }
+  // operator elements per T_PLR piece: one ring stage
+  int64_t t_piece_cap() const { return pp_.half_elems; }
 
   int emit_block(VecRef out, const std::vector<TermSpec>& terms,
                  const std::vector<EyeSpec>& eyes, bool has_init, VecRef init,
@@ -363,9 +359,8 @@ class Builder {
     for (size_t g = 0; g < groups_.size(); ++g)  // empty groups are complete at once
       if (gleft[g] == 0)
         for (int c : gcons_list[g]) --unmet[c];
-    // chain tasks first among the released ones: their latency is the
-    // launch's critical path, the rest fills in around them
-    auto prio = [&](int t) { return bl[t] + (task_chain_[t] ? pp_.chain_boost_us : 0.0); };
+    // (a queue-priority bonus for the sweeps' chain tasks measured slower)
+    auto prio = [&](int t) { return bl[t]; };
     for (int t = 0; t < n; ++t)
       if (unmet[t] == 0) ready.push(PI(prio(t), -t));
     std::vector<int> order;

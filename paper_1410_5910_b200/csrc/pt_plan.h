@@ -72,8 +72,6 @@ struct PlanParams {
   int t_pieces = 2;              // ring-stage pieces per T_PLR task
   int t_pieces_chain = 1;        // ... in the sweeps' dependency chain
   int row_chunk = ROW_CHUNK;     // output rows published per producer group
-  double chain_boost_us = 0.0;   // queue priority bonus of sweep-chain tasks
-  int64_t chain_piece_elems = 0; // T_PLR piece cap on the sweep chain (0: a stage)
   int64_t item_cap = 1 << 20;    // metadata items a task slot holds
   int max_block_terms = 0;       // A-apply: kernel terms per output task (0: all; else a block row is
                                  // emitted as partial sums of at most this many terms: smaller task slots)
