@@ -31,7 +31,7 @@ from ..cache import read_case, write_case
 from .assemble import extrapolator, extrapolator_pairs, polarized_rhs, polarized_table
 from .compress import leaf_table, plr_leaves
 from .configs import config
-from .layers import Layer, edge_extend, equal_partition
+from .layers import Layer, edge_extend, equal_partition, layer_operator
 
 ROOT = Path(__file__).resolve().parents[2]
 GOLDEN = ROOT / "tests" / "golden"
@@ -67,11 +67,85 @@ def _layer_job(job):
     return job["ell"], out, newtons, {"factor": t1 - t0, "greens": t2 - t1, "compress": t3 - t2}
 
 
+def _factor_job(job):
+    """Worker (GPU offline): the layer operator factored in the device order."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        pass
+    from .local import factor_layer
+    t0 = time.perf_counter()
+    op = layer_operator(job["nx"], job["n_layer"], job["h"], job["n_pml"], job["omega"], job["m_tilde"])
+    fac = factor_layer(op, job["n_layer"] + 2 * job["n_pml"], job["nx"] + 2 * job["n_pml"], check=False)
+    return job["ell"], fac, time.perf_counter() - t0
+
+
+def _compress_job(args):
+    """Worker (GPU offline): quadtree compression of one layer's blocks on the host."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        pass
+    blocks, r_max, eps = args
+    t0 = time.perf_counter()
+    out = {p: plr_leaves(b, r_max=r_max, eps=eps) for p, b in blocks.items()}
+    return out, time.perf_counter() - t0
+
+
+def _layer_job_gpu(job, fac, device, compress_on="cuda"):
+    """One layer on the GPU (offline.gpu): Green's blocks by multi-column
+    sparse triangular solves, Newton traces by the same factors, and (with
+    compress_on="cuda") PLR compression by batched SVDs; otherwise the dense
+    blocks of the kernels that need compression are returned under
+    "to_compress" for the host workers.  Same outputs as _layer_job."""
+    import torch
+    from .gpu import DeviceLayer, plr_leaves_gpu
+    nze, nxe = job["n_layer"] + 2 * job["n_pml"], job["nx"] + 2 * job["n_pml"]
+    t1 = time.perf_counter()
+    lay = DeviceLayer(fac, nze, nxe, job["n_layer"], job["n_pml"], job["h"], device)
+    blocks = lay.greens(job["pairs"])
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    out = {}
+    if job["compression"] is None:
+        for (j, k) in job["kernel_pairs"]:
+            out[(j, k)] = blocks[(j, k)].cpu().numpy()
+    elif compress_on == "cuda":
+        leaves = plr_leaves_gpu([blocks[p] for p in job["kernel_pairs"]],
+                                r_max=job["compression"][1], eps=job["compression"][0])
+        for p, lv in zip(job["kernel_pairs"], leaves):
+            out[p] = lv
+    else:
+        out["to_compress"] = {p: blocks[p].cpu().numpy() for p in job["kernel_pairs"]}
+    for d in job["extrapolators"]:  # dense, never compressed (trace_system.py:460-464)
+        num, den = extrapolator_pairs(job["n_layer"], d)
+        out[("E", d)] = extrapolator(blocks[num].cpu().numpy(), blocks[den].cpu().numpy())
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    newtons = []
+    n = job["n_layer"]
+    q_in = lay.inv_in.argsort()
+    for f in job["f_local"]:
+        b = torch.from_numpy(np.ascontiguousarray(f, dtype=np.complex128).ravel()).to(lay.device)
+        z = lay.solve_columns(b[q_in].unsqueeze(1))[:, 0]  # y = b[q_in]
+        w = z[lay.q_out].reshape(nze, nxe)
+        newtons.append({k: w[lay.row(k), :].cpu().numpy().copy() for k in (0, 1, n, n + 1)})
+    del lay, blocks
+    return job["ell"], out, newtons, {"greens": t2 - t1, "compress": t3 - t2}
+
+
 # cases whose operator is another case's (same medium and layering)
 OPERATOR_OF = {"c5": "c2"}
 
 
-def build_operator(name, workers=None, sources=True):
+def build_operator(name, workers=None, sources=True, device=None, compress_on="host"):
+    """``device`` (e.g. "cuda"): Green's extraction on the GPU (offline.gpu), the
+    layer factorizations on the host workers, the PLR compression on the host
+    workers as the blocks arrive (``compress_on="host"``) or by batched SVDs on
+    the GPU (``"cuda"``: same leaves, but cuSOLVER's complex128 SVD of the large
+    quadtree nodes is slower than the host workers)."""
     cfg = config(name)
     kernels_needed = name not in OPERATOR_OF
     g, L = cfg.geo, cfg.L
@@ -102,7 +176,41 @@ def build_operator(name, workers=None, sources=True):
                      "compression": cfg.compression, "f_local": f_local})
     workers = workers or min(L, os.cpu_count() or 1)
     t0 = time.perf_counter()
-    if workers > 1:
+    if device is not None:
+        # host workers factor the layers (in order), the GPU takes each layer
+        # as its factors arrive, and the workers compress the layer's blocks
+        # while the GPU extracts the next layer's
+        results, pending = [], []
+
+        def finish(r, compress):
+            blocks = r[1].pop("to_compress", None)
+            if blocks is not None:
+                args = (blocks, cfg.compression[1], cfg.compression[0])
+                pending.append((r, compress(args)))
+            results.append(r)
+
+        if workers > 1:
+            import multiprocessing as mp
+            ctx = mp.get_context("fork")
+            with ctx.Pool(min(workers, L)) as pool:
+                for ell, fac, t_fac in pool.imap(_factor_job, jobs, chunksize=1):
+                    r = _layer_job_gpu(jobs[ell - 1], fac, device, compress_on)
+                    r[3]["factor"] = t_fac
+                    finish(r, lambda a: pool.apply_async(_compress_job, (a,)))
+                for r, fut in pending:
+                    leaves, t_c = fut.get()
+                    r[1].update(leaves)
+                    r[3]["compress"] += t_c
+        else:
+            for job in jobs:
+                ell, fac, t_fac = _factor_job(job)
+                r = _layer_job_gpu(job, fac, device, compress_on)
+                r[3]["factor"] = t_fac
+                finish(r, _compress_job)
+            for r, (leaves, t_c) in pending:
+                r[1].update(leaves)
+                r[3]["compress"] += t_c
+    elif workers > 1:
         import multiprocessing as mp
         ctx = mp.get_context("fork")
         with ctx.Pool(min(workers, L)) as pool:
@@ -123,7 +231,8 @@ def build_operator(name, workers=None, sources=True):
             "offline_seconds": wall, "offline_workers": workers,
             "offline_stage_seconds": {k: float(sum(v[2][k] for v in per_layer.values()))
                                       for k in ("factor", "greens", "compress")},
-            "generator": "paper_1410_5910_b200.offline.build (restated reference offline)"}
+            "generator": "paper_1410_5910_b200.offline.build (restated reference offline" +
+                         (f"; Green's extraction and compression on {device})" if device else ")")}
     if not kernels_needed:
         meta["operator_case"] = OPERATOR_OF[name]
         del arrays["entries"], arrays["coefs"], arrays["perm"]
@@ -222,7 +331,9 @@ def build_case(name, out_dir=None, workers=None, verify=True):
     if name in OPERATOR_OF:
         ensure_case(OPERATOR_OF[name], out_dir, workers)
     t0 = time.perf_counter()
-    meta, arrays = build_operator(name, workers=workers)
+    # PT_OFFLINE_DEVICE=cuda: Green's extraction on the GPU (offline.gpu); the
+    # reference-checksum gate below applies either way
+    meta, arrays = build_operator(name, workers=workers, device=os.environ.get("PT_OFFLINE_DEVICE") or None)
     ref_path = GOLDEN / f"{name}_ref.ptc"
     if ref_path.exists():
         rmeta, rarr = read_case(ref_path, mmap=False)

@@ -22,25 +22,56 @@ def _svd_leaf(block, eps):
 
 
 def plr_leaves(block, r_max, eps):
-    """[(row_off, col_off, U (rows x r), Vt (r x cols))] in preorder."""
+    """[(row_off, col_off, U (rows x r), Vt (r x cols))] in preorder.
+
+    The split rule is the reference's (sigma_{r_max+1}(node) >= eps), evaluated
+    without the node's own SVD where a quadrant already decides it: the
+    singular values of a submatrix never exceed the matrix's
+    (sigma_k(B[I, J]) <= sigma_k(B)), so a quadrant with sigma_{r_max+1} >= eps
+    certifies the split -- and that quadrant's singular values are exactly what
+    its own decision needs next.  Only nodes no quadrant certifies (the ones
+    that end as leaves, mostly) get their own SVD.  Same leaves; the large
+    nodes near the root, which always split, cost nothing."""
     block = np.asarray(block, dtype=np.complex128)
     if block.ndim != 2 or block.size == 0:
         raise ValueError("block must be a nonempty 2D array")
     if r_max < 1 or not eps > 0:
         raise ValueError("need r_max >= 1 and epsilon > 0")
+    svals = {}
+
+    def sigma(r0, c0, b):  # singular values of the node at (r0, c0), memoised
+        key = (r0, c0, b.shape)
+        if key not in svals:
+            svals[key] = np.linalg.svd(b, compute_uv=False)
+        return svals[key]
+
+    def quadrants(r0, c0, b):
+        m, k = b.shape
+        rs, cs = m // 2, k // 2
+        return [(r0, c0, b[:rs, :cs]), (r0, c0 + cs, b[:rs, cs:]),
+                (r0 + rs, c0, b[rs:, :cs]), (r0 + rs, c0 + cs, b[rs:, cs:])]
+
+    def splits(r0, c0, b):
+        m, k = b.shape
+        if min(m, k) <= 2 * r_max:
+            return False
+        key = (r0, c0, b.shape)
+        if key not in svals:
+            for q in quadrants(r0, c0, b):
+                if min(q[2].shape) > r_max and sigma(*q)[r_max] >= eps:
+                    return True
+        return bool(sigma(r0, c0, b)[r_max] >= eps)
+
     out = []
     stack = [(0, 0, block)]
     while stack:
         r0, c0, b = stack.pop()
-        m, k = b.shape
-        if min(m, k) > 2 * r_max and np.linalg.svd(b, compute_uv=False)[r_max] >= eps:
-            rs, cs = m // 2, k // 2
+        if splits(r0, c0, b):
             # push in reverse so the pops come out TL, TR, BL, BR (preorder)
-            stack.append((r0 + rs, c0 + cs, b[rs:, cs:]))
-            stack.append((r0 + rs, c0, b[rs:, :cs]))
-            stack.append((r0, c0 + cs, b[:rs, cs:]))
-            stack.append((r0, c0, b[:rs, :cs]))
+            stack.extend(reversed(quadrants(r0, c0, b)))
+            svals.pop((r0, c0, b.shape), None)
             continue
+        svals.pop((r0, c0, b.shape), None)
         u, vt = _svd_leaf(b, eps)
         if u.shape[1]:
             out.append((r0, c0, u, vt))

@@ -275,6 +275,32 @@ def test_large_case_parity(cuda_ok, name):
 
 
 @pytest.mark.slow
+def test_c4_parity_against_the_reference(cuda_ok):
+    """c4 (1600 x 800, L = 32, PLR): the operator comes from the restated offline
+    stage, gated on the reference's own layer pipeline at three layers
+    (tests/golden/c4_ref.ptc, tools/make_c4_ref.py); the checks are the
+    reference's own applies (every 16th entry and the norms of A x and M x on
+    the seeded probe) and its own gmres_solve on that operator."""
+    meta, arr, op = get("c4", big=True)
+    assert meta.get("verified_against_reference"), "c4 operator not gated on the reference"
+    N = 2 * int(meta["nt"]) * int(meta["m"])
+    rng = np.random.default_rng(1234)
+    px = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    step = 16
+    for got, sub, nrm in ((op.apply_A(px), arr["probe_Ax_sub"], arr["probe_Ax_norm"]),
+                          (op.apply_M(px), arr["probe_Mx_sub"], arr["probe_Mx_norm"])):
+        got = np.asarray(got)
+        assert rel(got[::step], np.asarray(sub)) <= APPLY_TOL
+        assert abs(np.linalg.norm(got) - float(np.asarray(nrm)[0])) <= APPLY_TOL * float(np.asarray(nrm)[0])
+    ref = meta["solves"][0]
+    x, rep = op.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"], max_iter=100)
+    assert abs(rep["iterations"] - ref["iterations"]) <= 1
+    nt, m = meta["nt"], meta["m"]
+    assert rel(x[: nt * m] + x[nt * m:], arr["ref_traces"][0]) <= TRACE_TOL
+    del _OPS["c4"]  # 2.4 GB of factors
+
+
+@pytest.mark.slow
 def test_c5_batch_parity(cuda_ok):
     meta, arr, op = get("c5", big=True)
     nt, m = meta["nt"], meta["m"]
