@@ -358,18 +358,6 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
       const int n = t.c1 - t.c0;
       for (int c = lane; c < n; c += 32) sl.vec[c] = cadd(sl.vec[c], sl.vec[n + c]);
     }
-  } else if (t.type == TASK_Y_PLR) {  // dense-leaf columns: scale * (x_a + x_b)
-    const DevSrcRun* sr = sl.sruns();
-    for (int i = 0; i < t.nsrun; ++i) {
-      const DevSrcRun r = sr[i];
-      const double2 sc = sl.coef[r.term];
-      const bool two = sl.src[2 * r.term + 1] != nullptr;
-      for (int c = lane; c < r.n; c += 32) {
-        double2 v = sl.vec[r.f + c];
-        if (two) v = cadd(v, sl.vec[t.nitem + r.b_off + c]);
-        sl.vec[r.f + c] = cmul(sc, v);
-      }
-    }
   } else if (t.type == TASK_Y_DENSE) {
     for (int it = 0; it < t.nterm; ++it)
       if (sl.src[2 * it + 1])
@@ -614,6 +602,23 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
   constexpr int G = CONSUMERS / PLR_TILE;
   const int r = threadIdx.x % PLR_TILE, g = threadIdx.x / PLR_TILE;
   const DevItem* items = sl.items();
+  if (t.nsrun > 0) {
+    // dense-leaf columns: the staged source values become scale * (x_a + x_b)
+    // (by all consumer threads: a dense kernel's task stages ~1,000 of them,
+    // too many for the producer warp's serial pass on the dependency path)
+    const DevSrcRun* sr = sl.sruns();
+    for (int i = 0; i < t.nsrun; ++i) {
+      const DevSrcRun r = sr[i];
+      const double2 sc = sl.coef[r.term];
+      const bool two = sl.src[2 * r.term + 1] != nullptr;
+      for (int c = threadIdx.x; c < r.n; c += CONSUMERS) {
+        double2 v = sl.vec[r.f + c];
+        if (two) v = cadd(v, sl.vec[t.nitem + r.b_off + c]);
+        sl.vec[r.f + c] = cmul(sc, v);
+      }
+    }
+    consumer_sync();
+  }
   double2 acc = make_double2(0.0, 0.0);
   double2 acc2 = make_double2(0.0, 0.0);
   for (int p = 0; p < t.npiece; ++p) {

@@ -371,6 +371,37 @@ def test_scheduling_variants_bitwise_equal(cuda_ok, monkeypatch, name, variant):
         op2.close()
 
 
+STORAGE_VARIANTS = {
+    # dense kernels row-major through the 4-row split-K tasks (the default
+    # streams them tile-major through the 16-row tasks of the PLR path)
+    "row_major_dense": {"PT_DENSE_TILES": "0"},
+    # A-apply block rows as in-place partial sums of two kernel terms
+    "two_term_rows": {"PT_BLOCK_TERMS": "2"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(STORAGE_VARIANTS))
+@pytest.mark.parametrize("name", ["fx_tiny", "fx_uneven", "fx_plr", "fx_extrap_plr", "fx_extrap"])
+def test_storage_variants_match_the_reference(cuda_ok, monkeypatch, name, variant):
+    """Other operator storage / task partitions change the summation order,
+    not the result: every apply still meets the reference bar, and agrees
+    with the default executor to rounding."""
+    meta, arr, op = get(name)
+    for k, v in STORAGE_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    m2, a2 = load_case_arrays(golden_path(name))
+    op2 = DeviceOperator.from_arrays(m2, a2)
+    try:
+        x = np.asarray(arr["probe_x"])
+        assert rel(op2.apply_A(x), arr["probe_Ax"]) <= APPLY_TOL
+        assert rel(op2.apply_M(x, n_it=2), arr["probe_Mx"]) <= APPLY_TOL
+        assert rel(op2.apply_AM(x, n_it=2), op.apply_AM(x, n_it=2)) <= APPLY_TOL
+        xs, rep = op2.gmres(arr["rhs"][0], rel_tol=meta["gmres_tol"])
+        assert abs(rep["iterations"] - meta["solves"][0]["iterations"]) <= 1
+    finally:
+        op2.close()
+
+
 @pytest.mark.parametrize("name", ["fx_plr", "fx_extrap"])
 def test_one_handle_on_two_streams(cuda_ok, name):
     """Launches of one handle on different streams are ordered (they share the

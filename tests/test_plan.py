@@ -85,6 +85,19 @@ def test_dense_leaves_only_remove_bytes(monkeypatch):
     assert on["y_plr"] == off["y_plr"] and on["t_plr"] <= off["t_plr"]
 
 
+@pytest.mark.parametrize("name", FIXTURES)
+def test_partial_sum_block_rows_keep_the_bytes(monkeypatch, name):
+    """PT_BLOCK_TERMS=2 splits a block row's kernel terms over partial-sum
+    tasks: more output tasks, fewer terms each, the same operator bytes."""
+    whole = host_op(name).plan_stats("A")
+    monkeypatch.setenv("PT_BLOCK_TERMS", "2")
+    split = host_op(name).plan_stats("A")
+    assert split["staged_bytes"] == whole["staged_bytes"]
+    assert split["algo_bytes"] == whole["algo_bytes"]
+    assert split["max_terms"] <= 2
+    assert split["y_plr"] >= whole["y_plr"]
+
+
 def test_plan_only_handle_refuses_device_work():
     op = host_op(FIXTURES[0])
     x = np.zeros(op.N * 2)

@@ -69,7 +69,7 @@ def main():
         best, arg = 0.0, None
         for i in range(8):
             c, v = int(plan[q, 8 + 2 * i]), int(plan[q, 9 + 2 * i])
-            if c < 0:
+            if c < 0 or v <= 0:  # no wait / an empty producer group (dense kernels have no T tasks)
                 continue
             if v - 1 >= len(by_ctr.get(c, [])):
                 raise SystemExit(f"task {q}: wait ({c}, {v}) but counter has "
