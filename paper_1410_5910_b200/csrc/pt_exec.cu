@@ -294,8 +294,9 @@ __device__ __forceinline__ void parse_meta(const DevTask& t, const Slot& sl, int
 // The vector inputs of task t, after its dependencies (all 32 lanes): TMA
 // bulk copies of contiguous ranges (source slices, t-value runs, epilogue
 // rows) completing on the slot's staging barrier, all in flight at once.  A
-// merged term's second source lands right after the first and is added in
-// place (x_a + x_b, as the reference sums before applying the kernel).
+// merged term's second source lands right after the first; the consumers add
+// it in place when they start the task (x_a + x_b, as the reference sums
+// before applying the kernel; dense Y_DENSE terms are added here).
 __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& t, const Slot& sl,
                                               int k, int& n_staged, int lane) {
   const int nrows = t.r1 - t.r0;
@@ -353,12 +354,7 @@ __device__ __forceinline__ void stage_vectors(const ExecArgs& a, const DevTask& 
   __syncwarp();
   if (lane == 0) bar_arrive(&s_stg[k]);
   bar_wait(&s_stg[k], phase);
-  if (t.type == TASK_T_PLR) {
-    if (sl.src[1]) {
-      const int n = t.c1 - t.c0;
-      for (int c = lane; c < n; c += 32) sl.vec[c] = cadd(sl.vec[c], sl.vec[n + c]);
-    }
-  } else if (t.type == TASK_Y_DENSE) {
+  if (t.type == TASK_Y_DENSE) {
     for (int it = 0; it < t.nterm; ++it)
       if (sl.src[2 * it + 1])
         for (int c = lane; c < m; c += 32)
@@ -533,6 +529,11 @@ __device__ __forceinline__ void run_t_plr(const ExecArgs& a, const DevTask& t, c
   double2* T = s_slot[SLOT_T];
   const double2 sc = sl.coef[0];
   const DevItem* items = sl.items();
+  if (sl.src[1]) {  // merged term: the staged slices become x_a + x_b (all consumer threads)
+    const int n = t.c1 - t.c0;
+    for (int c = threadIdx.x; c < n; c += CONSUMERS) sl.vec[c] = cadd(sl.vec[c], sl.vec[n + c]);
+    consumer_sync();
+  }
   for (int p = 0; p < t.npiece; ++p) {
     const DevPiece& pc = sl.pieces()[p];
     const int n32 = pc.e0 & 1023, n16 = (pc.e0 >> 10) & 1023, n8 = (pc.e0 >> 20) & 1023;
