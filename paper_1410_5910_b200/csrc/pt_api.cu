@@ -150,6 +150,7 @@ struct pt_handle {
   int64_t slot_bytes = 0;  // bytes of one task slot
   int n_stages = 4;        // operator ring stages
   int n_slots = EXEC_TSLOTS;  // task slots in use per CTA
+  int piece_cap = EXEC_PIECES;  // operator pieces of one task the slot's blob area holds
   int api_fmt = 0;         // the kernel format pt_create was given (op.fmt is the executor's storage)
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
   // Launch ordering across streams: every program launch shares the handle's
@@ -525,9 +526,9 @@ int ensure_slot(pt_handle* h, int s, int64_t elems) {
 // each section 16-byte aligned.  In the blob copy of the DevTask, piece0 /
 // term0 / eye0 / wait0 / run0 / srun0 / item0 are byte offsets of the sections and
 // q is the queue index.
-int64_t blob_bytes_max(int64_t item_cap, int64_t run_cap, int64_t srun_cap) {
+int64_t blob_bytes_max(int64_t item_cap, int64_t run_cap, int64_t srun_cap, int64_t piece_cap = EXEC_PIECES) {
   auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
-  return al(sizeof(DevTask)) + al(EXEC_PIECES * sizeof(DevPiece)) + al(EXEC_TERMS * sizeof(DevTerm)) +
+  return al(sizeof(DevTask)) + al(piece_cap * sizeof(DevPiece)) + al(EXEC_TERMS * sizeof(DevTerm)) +
          al(EXEC_EYES * sizeof(DevEye)) + al(EXEC_WAITS * sizeof(DevWait)) +
          al(run_cap * (int64_t)sizeof(DevRun)) + al(srun_cap * (int64_t)sizeof(DevSrcRun)) +
          al(item_cap * (int64_t)sizeof(DevItem));
@@ -576,7 +577,7 @@ int check_slots(const pt_handle* h, const Program& pg) {
     if (t.type == TASK_Y_DENSE) vec = 2 * (int64_t)t.nterm * h->op.m;
     const int rows = t.type == TASK_Y_DENSE ? DENSE_RT_MAX : EXEC_EPI;
     if (vec > h->src_cap || t.nitem > h->item_cap || t.nterm > EXEC_TERMS ||
-        t.neye > EXEC_EYES || t.npiece > EXEC_PIECES ||
+        t.neye > EXEC_EYES || t.npiece > h->piece_cap ||
         t.nwait > EXEC_WAITS ||
         t.nrun > h->run_cap || t.nsrun > h->srun_cap ||
         (t.type != TASK_T_PLR && t.r1 - t.r0 > rows))
@@ -1050,6 +1051,9 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   h->pp.plr_slots_per_task = MAX_T_SLOTS;
   if (op.fmt == PT_KERNEL_DENSE) h->pp.item_cap = 0;
   h->pp.t_pieces = 4;
+  // a ring stage of a Y task may hold two terms' columns (PT_PIECE_PAIRS=0: one term per piece)
+  h->pp.piece_pairs = true;
+  if (const char* e = std::getenv("PT_PIECE_PAIRS")) h->pp.piece_pairs = std::atoi(e) != 0;
   if (const char* e = std::getenv("PT_DENSE_ROWS"))
     h->pp.dense_rows_per_task = std::max(1, std::min(DENSE_RT_MAX, std::atoi(e)));
   if (const char* e = std::getenv("PT_T_SLOTS")) h->pp.plr_slots_per_task = std::max(1, std::atoi(e));
@@ -1063,6 +1067,32 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     CK(cudaHostAlloc(&h->chk_host, 4 * sizeof(long long), cudaHostAllocMapped));
     std::memset(h->chk_host, 0, 4 * sizeof(long long));
     CK(cudaHostGetDevicePointer(&h->chk_dev, h->chk_host, 0));
+  }
+  {
+    // Second pass: the blob area reserved EXEC_PIECES piece descriptors per
+    // task; the operator's programs need far fewer (c3: 4), and what is saved
+    // goes to the ring stages.  A larger stage never splits a task into more
+    // pieces, so the maximum found with the first-pass stage holds.
+    int maxp = 1;
+    for (const Program& pg : {build_apply_A(op, h->pp), build_apply_M(op, 2, h->pp), build_gs_sweep(op, h->pp)})
+      for (const DevTask& t : pg.tasks) maxp = std::max(maxp, (int)t.npiece);
+    const int cap = std::min(EXEC_PIECES, std::max(8, maxp + 2));
+    const int64_t blob2 = (blob_bytes_max(h->item_cap, h->run_cap, h->srun_cap, cap) + 127) / 128 * 128;
+    if (cap < h->piece_cap && blob2 < h->blob_cap && maxp <= EXEC_PIECES) {
+      const int64_t slot2 = h->slot_bytes - (h->blob_cap - blob2);
+      const int64_t fixed2 = (int64_t)h->n_slots * slot2 + EXEC_PART * (int64_t)sizeof(double2);
+      const int64_t half2 = std::min<int64_t>(
+          65528, ((int64_t)h->smem - fixed2) / h->n_stages / (int64_t)sizeof(double2) / 8 * 8);
+      if (half2 >= h->pp.half_elems) {
+        h->piece_cap = cap;
+        h->blob_cap = blob2;
+        h->slot_bytes = slot2;
+        h->pp.half_elems = half2;
+        if (op.fmt == PT_KERNEL_DENSE && !std::getenv("PT_DENSE_ROWS"))
+          h->pp.dense_rows_per_task = (int)std::max<int64_t>(
+              1, std::min<int64_t>(DENSE_RT_MAX, half2 / std::max<int64_t>(op.m, 1)));
+      }
+    }
   }
   *out = h.release();
   return 0;
@@ -2026,7 +2056,7 @@ int pt_plan_stats(pt_handle* h, int32_t kind, int32_t n_it, int64_t* stats) {
   stats[5] = (int64_t)pg.items.size();
   stats[6] = pg.n_counters;
   stats[7] = (int64_t)pg.algo_bytes;
-  for (const DevPiece& pc : pg.pieces) stats[8] += 16 * (int64_t)pc.elems;
+  for (const DevPiece& pc : pg.pieces) stats[8] += 16 * (int64_t)(pc.elems + pc.elems2);
   if (!pg.overflow.empty()) return fail(PT_EINVAL, pg.overflow);
   return 0;
 }
@@ -2054,7 +2084,7 @@ int pt_plan_tasks(pt_handle* h, int32_t kind, int32_t n_it, int32_t* rec, int64_
     r[4] = t.r0;
     r[5] = t.r1;
     int64_t elems = 0;  // operator elements the task stages
-    for (int32_t i = 0; i < t.npiece; ++i) elems += pg.pieces[t.piece0 + i].elems;
+    for (int32_t i = 0; i < t.npiece; ++i) elems += pg.pieces[t.piece0 + i].elems + pg.pieces[t.piece0 + i].elems2;
     r[6] = t.out.slot | (t.nitem << 8);
     r[7] = (int32_t)elems;
     for (int i = 0; i < 8; ++i) {

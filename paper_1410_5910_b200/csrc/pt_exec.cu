@@ -239,15 +239,19 @@ __device__ __forceinline__ void issue_piece(const ExecArgs& a, const Layout& L, 
                                             int q, int p, uint32_t pos) {
   const DevPiece& pc = sl.pieces()[p];
   const int s = pos % (uint32_t)L.n_stages;
-  const uint32_t bytes = (uint32_t)pc.elems * (uint32_t)sizeof(double2);
-  CHK(pc.elems > 0 && pc.elems <= a.half_elems, CHK_PIECE_SIZE, q, pc.elems);
+  const uint32_t bytes = (uint32_t)(pc.elems + pc.elems2) * (uint32_t)sizeof(double2);
+  CHK(pc.elems > 0 && pc.elems2 >= 0 && pc.elems + pc.elems2 <= a.half_elems, CHK_PIECE_SIZE, q, pc.elems);
+  CHK(pc.elems2 == 0 || (pc.src2 >= 0 && pc.src2 + pc.elems2 <= a.fac_elems), CHK_PIECE_RANGE, q, pc.src2);
   CHK(pc.src >= 0 && pc.src + pc.elems <=
                          (sl.desc().type == TASK_Y_DENSE ? a.dense_elems : a.fac_elems),
       CHK_PIECE_RANGE, q, pc.src);
   const double2* src = (sl.desc().type == TASK_Y_DENSE ? a.dense : a.fac) + pc.src;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   bar_expect(&s_full[s], bytes);
-  bulk_copy(L.stage(s), src, bytes, &s_full[s]);
+  bulk_copy(L.stage(s), src, (uint32_t)pc.elems * (uint32_t)sizeof(double2), &s_full[s]);
+  if (pc.elems2 > 0)  // the second range (next term's columns) right behind the first
+    bulk_copy(L.stage(s) + pc.elems, a.fac + pc.src2, (uint32_t)pc.elems2 * (uint32_t)sizeof(double2),
+              &s_full[s]);
   if (p < 8) trace_mark(a, q, 14 + p);
 }
 

@@ -219,11 +219,18 @@ class Builder {
         tk.run0 = (int32_t)prog_.runs.size();
         tk.srun0 = (int32_t)prog_.sruns.size();
         int32_t f = 0, dense2 = 0;
+        // A piece is one ring stage: a contiguous range of the tile's columns
+        // of one term, and, where it fits, a second range (the next term's
+        // columns) right behind it (pp_.piece_pairs).
+        DevPiece pc{};
+        bool open = false, in_second = false;
         for (size_t it = 0; it < terms.size(); ++it) {
           const DevTerm& dt = prog_.terms[term0 + it];
           const int32_t k0 = op_.kplr[dt.kernel].tile0 + (int32_t)(r0 / PLR_TILE);
-          DevPiece pc{};
-          bool open = false;
+          bool first_of_term = true;
+          int64_t term_elems = 0;  // the term's columns of this tile
+          for (int32_t e = op_.tile_ptr[k0]; e < op_.tile_ptr[k0 + 1]; ++e)
+            term_elems += (int64_t)op_.tile_ent[e].rank * op_.tile_ent[e].stride;
           for (int32_t e = op_.tile_ptr[k0]; e < op_.tile_ptr[k0 + 1]; ++e) {
             const DevTileEntry& te = op_.tile_ent[e];
             if (te.rank > 0 && te.t0 >= 0) {  // t values from the term's T tasks
@@ -246,7 +253,15 @@ class Builder {
             }
             for (int32_t c = 0; c < te.rank; ++c, ++f) {
               const int64_t addr = te.u0 + (int64_t)c * te.stride;
-              if (open && pc.elems + te.stride > pp_.half_elems) {
+              // the open piece takes the column if it fits and continues one
+              // of its ranges -- or starts its second range (a new term)
+              const bool fits = open && pc.elems + pc.elems2 + te.stride <= pp_.half_elems;
+              const bool contiguous =
+                  open && addr == (in_second ? pc.src2 + pc.elems2 : pc.src + pc.elems);
+              // (a second range only for a term that fits whole: no fragments of large terms)
+              const bool second = open && !contiguous && first_of_term && !in_second &&
+                                  pp_.piece_pairs && pc.elems + term_elems <= pp_.half_elems;
+              if (open && !(fits && (contiguous || second))) {
                 prog_.pieces.push_back(pc);
                 open = false;
               }
@@ -255,19 +270,24 @@ class Builder {
                 pc.src = addr;
                 pc.f0 = f;
                 open = true;
+                in_second = false;
+              } else if (!contiguous) {
+                pc.src2 = addr;
+                in_second = true;
               }
+              first_of_term = false;
               DevItem item{};
-              item.poff = (uint16_t)pc.elems;
+              item.poff = (uint16_t)(pc.elems + pc.elems2);
               item.lo = (uint16_t)te.lo;
               item.hi = (uint16_t)te.hi;
               item.n = 0;
               prog_.items.push_back(item);
-              pc.elems += te.stride;
+              (in_second ? pc.elems2 : pc.elems) += te.stride;
               pc.f1 = f + 1;
             }
           }
-          if (open) prog_.pieces.push_back(pc);
         }
+        if (open) prog_.pieces.push_back(pc);
         tk.nitem = (int32_t)prog_.items.size() - tk.item0;
         tk.nrun = (int32_t)prog_.runs.size() - tk.run0;
         tk.nsrun = (int32_t)prog_.sruns.size() - tk.srun0;

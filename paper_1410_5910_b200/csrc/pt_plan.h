@@ -73,6 +73,7 @@ struct PlanParams {
   int t_pieces_chain = 1;        // ... in the sweeps' dependency chain
   int row_chunk = ROW_CHUNK;     // output rows published per producer group
   int64_t item_cap = 1 << 20;    // metadata items a task slot holds
+  bool piece_pairs = false;      // a Y_PLR ring stage may hold the columns of two terms (two ranges)
   int max_block_terms = 0;       // A-apply: kernel terms per output task (0: all; else a block row is
                                  // emitted as partial sums of at most this many terms: smaller task slots)
   bool force_dense = false;      // plan row-major dense tasks (Y_DENSE) whatever the operator's storage

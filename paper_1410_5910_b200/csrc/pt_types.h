@@ -68,6 +68,12 @@ struct DevPiece {
   int32_t elems;
   int32_t f0, f1;
   int32_t e0;
+  // Y_PLR: a second contiguous range that lands right behind the first in the
+  // same stage (the next term's columns of the tile: a stage filled by two
+  // terms instead of one piece per term)
+  int64_t src2;
+  int32_t elems2;
+  int32_t pad;
 };
 
 struct DevTask {
