@@ -66,6 +66,7 @@ struct DevProgram {
   DevTileEntry* ents = nullptr;
   DevPiece* pieces = nullptr;
   DevItem* items = nullptr;
+  bool fused = false;          // planned and launched with the handle's fused geometry
   int4* blob = nullptr;        // per-task metadata blobs (queue order)
   int64_t* blob_off = nullptr;  // task q: blob[blob_off[q] .. blob_off[q + 1])
   ~DevProgram() {
@@ -151,6 +152,27 @@ struct pt_handle {
   int n_stages = 4;        // operator ring stages
   int n_slots = EXEC_TSLOTS;  // task slots in use per CTA
   int piece_cap = EXEC_PIECES;  // operator pieces of one task the slot's blob area holds
+  // The executor geometry above (task-slot capacities, ring, plan parameters)
+  // is the default one: programs A, M, S.  The fused A -> M iteration has its
+  // own (PLR operators): its A-apply part is planned as short background
+  // tasks, which need smaller task slots and leave larger ring stages.
+  struct ExecGeom {
+    int64_t src_cap, item_cap, blob_cap, run_cap, srun_cap, slot_bytes;
+    int n_stages, n_slots, piece_cap, grid;
+    size_t smem;
+    PlanParams pp;
+  };
+  ExecGeom fused{};
+  bool has_fused = false;
+  ExecGeom geom() const {
+    return ExecGeom{src_cap, item_cap, blob_cap, run_cap, srun_cap, slot_bytes,
+                    n_stages, n_slots, piece_cap, grid, smem, pp};
+  }
+  void set_geom(const ExecGeom& g) {
+    src_cap = g.src_cap, item_cap = g.item_cap, blob_cap = g.blob_cap, run_cap = g.run_cap;
+    srun_cap = g.srun_cap, slot_bytes = g.slot_bytes, n_stages = g.n_stages, n_slots = g.n_slots;
+    piece_cap = g.piece_cap, grid = g.grid, smem = g.smem, pp = g.pp;
+  }
   int api_fmt = 0;         // the kernel format pt_create was given (op.fmt is the executor's storage)
   int poll_ns = 20;        // dependency-poll back-off (PT_POLL_NS)
   // Launch ordering across streams: every program launch shares the handle's
@@ -586,6 +608,28 @@ int check_slots(const pt_handle* h, const Program& pg) {
   return 0;
 }
 
+// The fused A -> M iteration's executor geometry while it is in scope.
+// Beside a sweep chain the A-apply is background work, and a chain task that
+// becomes ready waits for the background task its CTA's consumers are in:
+// short background tasks (block rows as two-term partial sums, T tasks of two
+// ring pieces) cost the A-apply alone ~20%, but they need smaller task slots,
+// which leaves larger ring stages, and shorten every sweep level (c3 GMRES
+// 17.46 -> 16.96 ms).  The stand-alone programs keep the default geometry.
+struct FusedGeom {
+  pt_handle* h;
+  pt_handle::ExecGeom saved;
+  bool on;
+  FusedGeom(pt_handle* h_, bool use) : h(h_), on(use && h_->has_fused) {
+    if (on) {
+      saved = h->geom();
+      h->set_geom(h->fused);
+    }
+  }
+  ~FusedGeom() {
+    if (on) h->set_geom(saved);
+  }
+};
+
 int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** out) {
   const std::string key = kind + std::to_string(n_it);
   auto it = h->progs.find(key);
@@ -594,6 +638,8 @@ int get_program(pt_handle* h, const std::string& kind, int n_it, DevProgram** ou
     return 0;
   }
   std::unique_ptr<DevProgram> p(new DevProgram());
+  p->fused = kind == "AM" && h->has_fused;
+  FusedGeom scope(h, p->fused);
   if (kind == "A")
     p->host = build_apply_A(h->op, h->pp);
   else if (kind == "M")
@@ -666,6 +712,7 @@ int order_after(pt_handle* h, cudaStream_t s) {
 int run_program(pt_handle* h, DevProgram* p, const double2* in, double2* out, const double2* aux,
                 cudaStream_t s, const int* stop = nullptr, IterMode im = IterMode()) {
   if (p->host.tasks.empty()) return 0;
+  FusedGeom scope(h, p->fused);
   ExecArgs a{};
   a.tasks = p->tasks;
   a.terms = p->terms;
@@ -861,64 +908,11 @@ int32_t pt_abi_version(void) { return PT_ABI_VERSION; }
 int64_t pt_launch_count(void) { return pt::g_launches.load(); }
 int32_t pt_checked_build(void) { return PT_CHECK; }
 
-int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entries,
-              const int64_t* perm, const double* dense, const pt_leaf* leaves, int64_t n_leaves,
-              const double* factors, int64_t n_factor_complex, int device, pt_handle** out) {
-  if (!layout || !out || (n_entries > 0 && !entries) || !perm)
-    return fail(PT_EINVAL, "null argument to pt_create");
-  *out = nullptr;
-  const bool host_only = device == PT_DEVICE_HOST;
-  if (!host_only) {
-    int ndev = 0;
-    CK(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return fail(PT_EINVAL, "no such CUDA device");
-  }
-  std::unique_ptr<DeviceGuard> guard(host_only ? nullptr : new DeviceGuard(device));
-  std::unique_ptr<pt_handle> h(new pt_handle());
-  h->device = device;
-  h->host_only = host_only;
-  if (const char* e = std::getenv("PT_DENSE_LEAVES")) h->dense_leaves = std::atoi(e) != 0;
+// Executor geometry of a handle from its operator and the plan parameters
+// already set in h->pp (max_block_terms; want_t_pieces): task-slot capacities,
+// ring stages, shared memory, grid, and the remaining plan parameters.
+int size_executor(pt_handle* h, bool host_only, int device, int want_t_pieces) {
   Operator& op = h->op;
-  op.m = layout->m;
-  op.nb = layout->n_block_rows;
-  op.fmt = layout->kernel_format;
-  op.nk = layout->n_kernels;
-  if (op.fmt != PT_KERNEL_DENSE && op.fmt != PT_KERNEL_PLR)
-    return fail(PT_EINVAL, "unknown kernel format");
-  if (op.nk < 0) return fail(PT_EINVAL, "negative kernel count");
-  if (op.m > (int64_t)1 << 20) return fail(PT_EINVAL, "block size too large");
-  op.perm.assign(perm, perm + std::max<int64_t>(layout->n_block_rows, 0));
-  for (int64_t i = 0; i < n_entries; ++i) {
-    const pt_entry& e = entries[i];
-    op.entries.push_back(HostEntry{e.row, e.col, e.kernel, e.scale_re, e.scale_im, e.eye_re, e.eye_im});
-  }
-  std::string err;
-  if (!validate_operator(op, err)) return fail(PT_EINVAL, err);
-  h->sweep_err = sweep_diagonal_error(op);
-  int rc;
-  h->api_fmt = op.fmt;
-  if (op.fmt == PT_KERNEL_DENSE) {
-    op.kernel_bytes.assign(op.nk, 16 * op.m * op.m);
-    if (op.nk > 0 && !host_only) {
-      if (!dense) return fail(PT_EINVAL, "dense kernel array missing");
-      const size_t bytes = (size_t)op.nk * op.m * op.m * sizeof(double2);
-      CK(cudaMalloc(&h->dense, bytes));
-      h->dense_elems = (int64_t)op.nk * op.m * op.m;
-      CK(cudaMemcpy(h->dense, dense, bytes, cudaMemcpyHostToDevice));
-    }
-    // the single-source executor streams dense kernels tile-major, as the
-    // dense leaves of a PLR kernel (PT_DENSE_TILES=0: row-major Y_DENSE tasks)
-    bool tiles = true;
-    if (const char* e = std::getenv("PT_DENSE_TILES")) tiles = std::atoi(e) != 0;
-    if (tiles) {
-      if ((rc = build_dense_tiles(h.get(), dense))) return rc;
-      op.fmt = PT_KERNEL_PLR;
-    }
-  } else {
-    if (n_leaves > 0 && (!leaves || !factors)) return fail(PT_EINVAL, "PLR tables missing");
-    if ((rc = build_plr_tables(h.get(), leaves, n_leaves, factors, n_factor_complex))) return rc;
-  }
-  if (const char* e = std::getenv("PT_BLOCK_TERMS")) h->pp.max_block_terms = std::max(0, std::atoi(e));
   // Shared memory per CTA: [EXEC_STAGES operator ring stages][EXEC_TSLOTS task
   // slots: descriptor, items, staged vectors, epilogue rows, term scales]
   // [consumer partials].  The stages take what is left after the fixed part
@@ -1050,7 +1044,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   h->pp.plr_rows_per_task = PLR_TILE;
   h->pp.plr_slots_per_task = MAX_T_SLOTS;
   if (op.fmt == PT_KERNEL_DENSE) h->pp.item_cap = 0;
-  h->pp.t_pieces = 4;
+  h->pp.t_pieces = want_t_pieces;
   // a ring stage of a Y task may hold two terms' columns (PT_PIECE_PAIRS=0: one term per piece)
   h->pp.piece_pairs = true;
   if (const char* e = std::getenv("PT_PIECE_PAIRS")) h->pp.piece_pairs = std::atoi(e) != 0;
@@ -1062,12 +1056,6 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
   if (const char* e = std::getenv("PT_POLL_NS")) h->poll_ns = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
     h->pp.t_pieces_chain = std::max(1, std::atoi(e));
-  if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
-  if (!host_only && pt_checked_build()) {  // the executor's failure record (mapped host memory)
-    CK(cudaHostAlloc(&h->chk_host, 4 * sizeof(long long), cudaHostAllocMapped));
-    std::memset(h->chk_host, 0, 4 * sizeof(long long));
-    CK(cudaHostGetDevicePointer(&h->chk_dev, h->chk_host, 0));
-  }
   {
     // Second pass: the blob area reserved EXEC_PIECES piece descriptors per
     // task; the operator's programs need far fewer (c3: 4), and what is saved
@@ -1093,6 +1081,85 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
               1, std::min<int64_t>(DENSE_RT_MAX, half2 / std::max<int64_t>(op.m, 1)));
       }
     }
+  }
+  return 0;
+}
+
+int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entries,
+              const int64_t* perm, const double* dense, const pt_leaf* leaves, int64_t n_leaves,
+              const double* factors, int64_t n_factor_complex, int device, pt_handle** out) {
+  if (!layout || !out || (n_entries > 0 && !entries) || !perm)
+    return fail(PT_EINVAL, "null argument to pt_create");
+  *out = nullptr;
+  const bool host_only = device == PT_DEVICE_HOST;
+  if (!host_only) {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(PT_EINVAL, "no such CUDA device");
+  }
+  std::unique_ptr<DeviceGuard> guard(host_only ? nullptr : new DeviceGuard(device));
+  std::unique_ptr<pt_handle> h(new pt_handle());
+  h->device = device;
+  h->host_only = host_only;
+  if (const char* e = std::getenv("PT_DENSE_LEAVES")) h->dense_leaves = std::atoi(e) != 0;
+  Operator& op = h->op;
+  op.m = layout->m;
+  op.nb = layout->n_block_rows;
+  op.fmt = layout->kernel_format;
+  op.nk = layout->n_kernels;
+  if (op.fmt != PT_KERNEL_DENSE && op.fmt != PT_KERNEL_PLR)
+    return fail(PT_EINVAL, "unknown kernel format");
+  if (op.nk < 0) return fail(PT_EINVAL, "negative kernel count");
+  if (op.m > (int64_t)1 << 20) return fail(PT_EINVAL, "block size too large");
+  op.perm.assign(perm, perm + std::max<int64_t>(layout->n_block_rows, 0));
+  for (int64_t i = 0; i < n_entries; ++i) {
+    const pt_entry& e = entries[i];
+    op.entries.push_back(HostEntry{e.row, e.col, e.kernel, e.scale_re, e.scale_im, e.eye_re, e.eye_im});
+  }
+  std::string err;
+  if (!validate_operator(op, err)) return fail(PT_EINVAL, err);
+  h->sweep_err = sweep_diagonal_error(op);
+  int rc;
+  h->api_fmt = op.fmt;
+  if (op.fmt == PT_KERNEL_DENSE) {
+    op.kernel_bytes.assign(op.nk, 16 * op.m * op.m);
+    if (op.nk > 0 && !host_only) {
+      if (!dense) return fail(PT_EINVAL, "dense kernel array missing");
+      const size_t bytes = (size_t)op.nk * op.m * op.m * sizeof(double2);
+      CK(cudaMalloc(&h->dense, bytes));
+      h->dense_elems = (int64_t)op.nk * op.m * op.m;
+      CK(cudaMemcpy(h->dense, dense, bytes, cudaMemcpyHostToDevice));
+    }
+    // the single-source executor streams dense kernels tile-major, as the
+    // dense leaves of a PLR kernel (PT_DENSE_TILES=0: row-major Y_DENSE tasks)
+    bool tiles = true;
+    if (const char* e = std::getenv("PT_DENSE_TILES")) tiles = std::atoi(e) != 0;
+    if (tiles) {
+      if ((rc = build_dense_tiles(h.get(), dense))) return rc;
+      op.fmt = PT_KERNEL_PLR;
+    }
+  } else {
+    if (n_leaves > 0 && (!leaves || !factors)) return fail(PT_EINVAL, "PLR tables missing");
+    if ((rc = build_plr_tables(h.get(), leaves, n_leaves, factors, n_factor_complex))) return rc;
+  }
+  if (const char* e = std::getenv("PT_BLOCK_TERMS")) h->pp.max_block_terms = std::max(0, std::atoi(e));
+  if ((rc = size_executor(h.get(), host_only, device, 4))) return rc;
+  if (h->api_fmt == PT_KERNEL_PLR && !std::getenv("PT_BLOCK_TERMS") && !std::getenv("PT_T_PIECES")) {
+    // the fused iteration's geometry: block rows as two-term partial sums, T
+    // tasks of two ring pieces (see fused_params)
+    const pt_handle::ExecGeom base = h->geom();
+    h->pp.max_block_terms = 2;
+    h->run_cap = h->srun_cap = 0;
+    if ((rc = size_executor(h.get(), host_only, device, 2))) return rc;
+    h->fused = h->geom();
+    h->has_fused = true;
+    h->set_geom(base);
+  }
+  if (!host_only) CK(cudaMalloc(&h->tmp, std::max<int64_t>(h->N(), 1) * sizeof(double2)));
+  if (!host_only && pt_checked_build()) {  // the executor's failure record (mapped host memory)
+    CK(cudaHostAlloc(&h->chk_host, 4 * sizeof(long long), cudaHostAllocMapped));
+    std::memset(h->chk_host, 0, 4 * sizeof(long long));
+    CK(cudaHostGetDevicePointer(&h->chk_dev, h->chk_host, 0));
   }
   *out = h.release();
   return 0;
@@ -1441,6 +1508,8 @@ int get_bprogram(pt_handle* h, const std::string& kind, int n_it, DevProgram** o
     return 0;
   }
   std::unique_ptr<DevProgram> p(new DevProgram());
+  p->fused = kind == "AM" && h->has_fused;
+  FusedGeom scope(h, p->fused);
   if (kind == "A")
     p->host = build_apply_A(h->op, B.pp);
   else if (kind == "M")
@@ -2032,6 +2101,7 @@ int pt_plan_stats(pt_handle* h, int32_t kind, int32_t n_it, int64_t* stats) {
     if (!h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
   }
   if (kind == 3 && !h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  FusedGeom scope(h, kind == 2);
   Program pg = kind == 0   ? build_apply_A(h->op, h->pp)
                : kind == 1 ? build_apply_M(h->op, n_it, h->pp)
                : kind == 2 ? build_A_then_M(h->op, n_it, h->pp)
@@ -2067,6 +2137,7 @@ int pt_plan_tasks(pt_handle* h, int32_t kind, int32_t n_it, int32_t* rec, int64_
   if (kind < 0 || kind > 3) return fail(PT_EINVAL, "unknown program kind");
   if ((kind == 1 || kind == 2) && n_it < 1) return fail(PT_EINVAL, "n_it must be at least 1");
   if (kind != 0 && !h->sweep_err.empty()) return fail(PT_EINVAL, h->sweep_err);
+  FusedGeom scope(h, kind == 2);
   Program pg = kind == 0   ? build_apply_A(h->op, h->pp)
                : kind == 1 ? build_apply_M(h->op, n_it, h->pp)
                : kind == 2 ? build_A_then_M(h->op, n_it, h->pp)

@@ -80,8 +80,16 @@ def _fused_matches_separate(op, x):
     import torch
     xd = torch.from_numpy(np.array(x)).cuda()
     ref = op.apply_M(op.apply_A(xd))
+    first = op.apply_AM(xd).clone()
     for _ in range(8):  # a scheduling race would show up as a mismatch
-        assert torch.equal(op.apply_AM(xd), ref)
+        assert torch.equal(op.apply_AM(xd), first)
+    # the fused program sums a PLR block row's kernel terms as two partial sums
+    # (short background tasks beside the sweep chain): equal to the separate
+    # applies to rounding; a dense operator's fused program is the same tasks
+    if op.kernel_format == "dense":
+        assert torch.equal(first, ref)
+    else:
+        assert float(torch.linalg.norm(first - ref) / torch.linalg.norm(ref)) <= 1e-13
 
 
 @pytest.mark.parametrize("name", FIXTURES)
@@ -366,7 +374,12 @@ def test_scheduling_variants_bitwise_equal(cuda_ok, monkeypatch, name, variant):
         x = np.asarray(arr["probe_x"]) if "probe_x" in arr else np.asarray(arr["rhs"][0])
         assert np.array_equal(op.apply_A(x), op2.apply_A(x))
         assert np.array_equal(op.apply_M(x, n_it=2), op2.apply_M(x, n_it=2))
-        assert np.array_equal(op.apply_AM(x, n_it=2), op2.apply_AM(x, n_it=2))
+        # (PT_T_PIECES switches the fused program's own geometry off: its A part
+        # then sums a block row's terms in one task instead of two partial sums)
+        if op.kernel_format == "dense" or "PT_T_PIECES" not in VARIANTS[variant]:
+            assert np.array_equal(op.apply_AM(x, n_it=2), op2.apply_AM(x, n_it=2))
+        else:
+            assert rel(op2.apply_AM(x, n_it=2), op.apply_AM(x, n_it=2)) <= 1e-13
     finally:
         op2.close()
 
