@@ -1150,7 +1150,7 @@ int pt_create(const pt_layout* layout, const pt_entry* entries, int64_t n_entrie
     const pt_handle::ExecGeom base = h->geom();
     h->pp.max_block_terms = 2;
     h->run_cap = h->srun_cap = 0;
-    if ((rc = size_executor(h.get(), host_only, device, 2))) return rc;
+    if ((rc = size_executor(h.get(), host_only, device, 2))) return rc;  // (T pieces 1 / 3 measured: 17.75 / 17.05 ms)
     h->fused = h->geom();
     h->has_fused = true;
     h->set_geom(base);
