@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -548,9 +549,9 @@ int ensure_slot(pt_handle* h, int s, int64_t elems) {
 // each section 16-byte aligned.  In the blob copy of the DevTask, piece0 /
 // term0 / eye0 / wait0 / run0 / srun0 / item0 are byte offsets of the sections and
 // q is the queue index.
-int64_t blob_bytes_max(int64_t item_cap, int64_t run_cap, int64_t srun_cap, int64_t piece_cap = EXEC_PIECES) {
+int64_t blob_bytes_max(int64_t item_cap, int64_t run_cap, int64_t srun_cap) {
   auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
-  return al(sizeof(DevTask)) + al(piece_cap * sizeof(DevPiece)) + al(EXEC_TERMS * sizeof(DevTerm)) +
+  return al(sizeof(DevTask)) + al(EXEC_PIECES * sizeof(DevPiece)) + al(EXEC_TERMS * sizeof(DevTerm)) +
          al(EXEC_EYES * sizeof(DevEye)) + al(EXEC_WAITS * sizeof(DevWait)) +
          al(run_cap * (int64_t)sizeof(DevRun)) + al(srun_cap * (int64_t)sizeof(DevSrcRun)) +
          al(item_cap * (int64_t)sizeof(DevItem));
@@ -1057,31 +1058,51 @@ int size_executor(pt_handle* h, bool host_only, int device, int want_t_pieces) {
   if (const char* e = std::getenv("PT_T_PIECES_CHAIN"))
     h->pp.t_pieces_chain = std::max(1, std::atoi(e));
   {
-    // Second pass: the blob area reserved EXEC_PIECES piece descriptors per
-    // task; the operator's programs need far fewer (c3: 4), and what is saved
-    // goes to the ring stages.  A larger stage never splits a task into more
-    // pieces, so the maximum found with the first-pass stage holds.
-    int maxp = 1;
-    for (const Program& pg : {build_apply_A(op, h->pp), build_apply_M(op, 2, h->pp), build_gs_sweep(op, h->pp)})
-      for (const DevTask& t : pg.tasks) maxp = std::max(maxp, (int)t.npiece);
-    const int cap = std::min(EXEC_PIECES, std::max(8, maxp + 2));
-    const int64_t blob2 = (blob_bytes_max(h->item_cap, h->run_cap, h->srun_cap, cap) + 127) / 128 * 128;
-    if (cap < h->piece_cap && blob2 < h->blob_cap && maxp <= EXEC_PIECES) {
-      const int64_t slot2 = h->slot_bytes - (h->blob_cap - blob2);
-      const int64_t fixed2 = (int64_t)h->n_slots * slot2 + EXEC_PART * (int64_t)sizeof(double2);
-      const int64_t half2 = std::min<int64_t>(
-          65528, ((int64_t)h->smem - fixed2) / h->n_stages / (int64_t)sizeof(double2) / 8 * 8);
-      if (half2 >= h->pp.half_elems) {
-        h->piece_cap = cap;
-        h->blob_cap = blob2;
-        h->slot_bytes = slot2;
-        h->pp.half_elems = half2;
-        if (op.fmt == PT_KERNEL_DENSE && !std::getenv("PT_DENSE_ROWS"))
-          h->pp.dense_rows_per_task = (int)std::max<int64_t>(
-              1, std::min<int64_t>(DENSE_RT_MAX, half2 / std::max<int64_t>(op.m, 1)));
+    // Second pass: the blob area was reserved for the largest task the
+    // limits allow (EXEC_PIECES pieces, EXEC_TERMS terms, EXEC_WAITS waits);
+    // the operator's programs need far less, and what is saved goes to the
+    // ring stages.  The programs are planned again with the larger stage and
+    // must still fit (a larger stage packs a few more Vt rows into a T
+    // task); otherwise the first-pass geometry stays.
+    auto max_blob = [&](int64_t* mx) {
+      *mx = 0;
+      for (const Program& pg : {build_apply_A(op, h->pp), build_apply_M(op, 2, h->pp), build_gs_sweep(op, h->pp)}) {
+        if (!pg.overflow.empty()) return false;
+        std::vector<int4> blob;
+        std::vector<int64_t> off;
+        int64_t m1 = 0;
+        build_blobs(pg, blob, off, &m1);
+        *mx = std::max(*mx, m1);
+      }
+      return true;
+    };
+    int64_t mx = 0;
+    if (max_blob(&mx)) {
+      const int64_t blob2 = (mx + 512 + 127) / 128 * 128;
+      if (blob2 < h->blob_cap) {
+        const pt_handle::ExecGeom first = h->geom();
+        const int64_t slot2 = h->slot_bytes - (h->blob_cap - blob2);
+        const int64_t fixed2 = (int64_t)h->n_slots * slot2 + EXEC_PART * (int64_t)sizeof(double2);
+        const int64_t half2 = std::min<int64_t>(
+            65528, ((int64_t)h->smem - fixed2) / h->n_stages / (int64_t)sizeof(double2) / 8 * 8);
+        if (half2 > h->pp.half_elems) {
+          h->blob_cap = blob2;
+          h->slot_bytes = slot2;
+          h->pp.half_elems = half2;
+          if (op.fmt == PT_KERNEL_DENSE && !std::getenv("PT_DENSE_ROWS"))
+            h->pp.dense_rows_per_task = (int)std::max<int64_t>(
+                1, std::min<int64_t>(DENSE_RT_MAX, half2 / std::max<int64_t>(op.m, 1)));
+          int64_t mx2 = 0;
+          if (!max_blob(&mx2) || mx2 > blob2) h->set_geom(first);
+        }
       }
     }
   }
+  if (std::getenv("PT_VERBOSE"))
+    std::fprintf(stderr, "executor geometry: smem %zu B, %d slots x %lld B (blob %lld, vec %lld), %d stages x %lld B, block terms %d\n",
+                 h->smem, h->n_slots, (long long)h->slot_bytes, (long long)h->blob_cap,
+                 (long long)h->src_cap * 16, h->n_stages, (long long)h->pp.half_elems * 16,
+                 h->pp.max_block_terms);
   return 0;
 }
 
