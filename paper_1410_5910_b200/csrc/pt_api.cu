@@ -545,7 +545,7 @@ int ensure_slot(pt_handle* h, int s, int64_t elems) {
 // Per-task metadata blobs, in queue order, so a producer warp fetches a
 // task's whole description with one bulk copy:
 //   [DevTask][DevPiece x npiece][DevTerm x nterm][DevEye x neye]
-//   [DevWait x nwait][DevRun x nrun][DevSrcRun x nsrun][DevItem x nitem]
+//   [DevWait x nwait][DevRun x nrun][DevSrcRun x nsrun][DevItem x nitem (T) | packed uint32 x nitem (Y)]
 // each section 16-byte aligned.  In the blob copy of the DevTask, piece0 /
 // term0 / eye0 / wait0 / run0 / srun0 / item0 are byte offsets of the sections and
 // q is the queue index.
@@ -579,7 +579,17 @@ void build_blobs(const Program& pg, std::vector<int4>& blob, std::vector<int64_t
     d.wait0 = put(pg.waits.data() + t.wait0, (size_t)t.nwait * sizeof(DevWait));
     d.run0 = put(pg.runs.data() + t.run0, (size_t)t.nrun * sizeof(DevRun));
     d.srun0 = put(pg.sruns.data() + t.srun0, (size_t)t.nsrun * sizeof(DevSrcRun));
-    d.item0 = put(pg.items.data() + t.item0, (size_t)t.nitem * sizeof(DevItem));
+    if (t.type == TASK_Y_PLR) {
+      // a Y column's item in 4 bytes: offset in its stage | first tile row << 16 | end row << 20
+      std::vector<uint32_t> packed((size_t)t.nitem);
+      for (int32_t i = 0; i < t.nitem; ++i) {
+        const DevItem& it = pg.items[(size_t)t.item0 + i];
+        packed[i] = (uint32_t)it.poff | ((uint32_t)it.lo << 16) | ((uint32_t)it.hi << 20);
+      }
+      d.item0 = put(packed.data(), packed.size() * sizeof(uint32_t));
+    } else {
+      d.item0 = put(pg.items.data() + t.item0, (size_t)t.nitem * sizeof(DevItem));
+    }
     d.q = (int32_t)q;
     std::memcpy(b.data(), &d, sizeof(DevTask));
     *max_bytes = std::max<int64_t>(*max_bytes, (int64_t)b.size());

@@ -606,7 +606,8 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
                                           const Layout& L, Ring& rg, int q) {
   constexpr int G = CONSUMERS / PLR_TILE;
   const int r = threadIdx.x % PLR_TILE, g = threadIdx.x / PLR_TILE;
-  const DevItem* items = sl.items();
+  // a column's item: offset in its stage | first tile row << 16 | end row << 20
+  const uint32_t* items = reinterpret_cast<const uint32_t*>(sl.blob + t.item0);
   if (t.nsrun > 0) {
     // dense-leaf columns: the staged source values become scale * (x_a + x_b)
     // (by all consumer threads: a dense kernel's task stages ~1,000 of them,
@@ -631,18 +632,21 @@ __device__ __forceinline__ void run_y_plr(const ExecArgs& a, const DevTask& t, c
     const double2* buf = wait_piece(a, L, rg, q, p);
     int f = pc.f0 + ((g - pc.f0) % G + G) % G;
     for (; f + G < pc.f1; f += 2 * G) {
-      const DevItem i0 = items[f], i1 = items[f + G];
-      CHK(i0.poff + (i0.hi - i0.lo) <= a.half_elems && i1.poff + (i1.hi - i1.lo) <= a.half_elems &&
-              i0.hi <= PLR_TILE && i1.hi <= PLR_TILE, CHK_ITEM_RANGE, q, f);
+      const uint32_t w0 = items[f], w1 = items[f + G];
+      const int p0 = (int)(w0 & 0xFFFFu), lo0 = (int)((w0 >> 16) & 15u), hi0 = (int)((w0 >> 20) & 31u);
+      const int p1 = (int)(w1 & 0xFFFFu), lo1 = (int)((w1 >> 16) & 15u), hi1 = (int)((w1 >> 20) & 31u);
+      CHK(p0 + (hi0 - lo0) <= a.half_elems && p1 + (hi1 - lo1) <= a.half_elems &&
+              hi0 <= PLR_TILE && hi1 <= PLR_TILE, CHK_ITEM_RANGE, q, f);
       const double2 t0 = sl.vec[f], t1 = sl.vec[f + G];
-      const double2 u0 = r >= i0.lo && r < i0.hi ? buf[i0.poff + (r - i0.lo)] : make_double2(0.0, 0.0);
-      const double2 u1 = r >= i1.lo && r < i1.hi ? buf[i1.poff + (r - i1.lo)] : make_double2(0.0, 0.0);
+      const double2 u0 = r >= lo0 && r < hi0 ? buf[p0 + (r - lo0)] : make_double2(0.0, 0.0);
+      const double2 u1 = r >= lo1 && r < hi1 ? buf[p1 + (r - lo1)] : make_double2(0.0, 0.0);
       acc = cfma(u0, t0, acc);
       acc2 = cfma(u1, t1, acc2);
     }
     if (f < pc.f1) {
-      const DevItem it = items[f];
-      if (r >= it.lo && r < it.hi) acc = cfma(buf[it.poff + (r - it.lo)], sl.vec[f], acc);
+      const uint32_t w = items[f];
+      const int po = (int)(w & 0xFFFFu), lo = (int)((w >> 16) & 15u), hi = (int)((w >> 20) & 31u);
+      if (r >= lo && r < hi) acc = cfma(buf[po + (r - lo)], sl.vec[f], acc);
     }
     release_piece(L, rg);
   }
